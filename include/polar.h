@@ -1,0 +1,251 @@
+/*
+ * polar.h — C ABI of libpolar, a policy-selected AllReduce for B200 (sm_100a).
+ *
+ * The hot path is: a bounded tuner decision keyed by
+ * (collective, bytes, nranks) picks an algorithm, a protocol and a channel count
+ * (§2, §3.3), then ONE hand-written sm_100a kernel
+ * moves and reduces the data by reading/writing peer buffers directly
+ * (NVLink/NVSwitch peer mappings on a real node; the same kernels drive
+ * "virtual ranks" that share one GPU).
+ *
+ * Conventions for every function:
+ *   - Nothing aborts, throws or exits across this ABI; every call returns a
+ *     polar_status (or a plain value where documented).
+ *   - "device pointer" = memory on the comm's CUDA device (cudaMalloc /
+ *     torch); "host pointer" = ordinary process memory.
+ *   - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ *     default stream); kernels are enqueued asynchronously, no host sync.
+ *   - Collective functions must be called by every rank of the comm, in the same
+ *     order, with matching arguments (NCCL rules); one host thread per comm at a
+ *     time.  Policy functions are process-global and thread-safe.
+ *   - Errors raised on the device (a peer that never arrives) are latched in the
+ *     comm and returned by the NEXT call on it, or by polar_comm_check().
+ */
+#ifndef POLAR_H
+#define POLAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ enums */
+
+typedef enum {
+    POLAR_OK = 0,
+    POLAR_EINVAL = 1,        /* malformed argument or policy table                   */
+    POLAR_ECUDA = 2,         /* a CUDA runtime/driver call failed                     */
+    POLAR_EUNSUPPORTED = 3,  /* well-formed but not built (NVLS, LL128, other colls)  */
+    POLAR_ETIMEOUT = 4,      /* a device-side wait for a peer exceeded the timeout    */
+    POLAR_EBUSY = 5,         /* concurrent use of a single-threaded object            */
+    POLAR_ESTATE = 6,        /* comm unusable (earlier latched error / destroyed)     */
+    POLAR_ENOMEM = 7         /* device or host allocation failed                      */
+} polar_status;
+
+/* dtype / op use NCCL's numbering so one harness can drive both (nccl.h). */
+typedef enum { POLAR_INT32 = 2, POLAR_INT64 = 4, POLAR_FLOAT32 = 7, POLAR_BFLOAT16 = 9 } polar_dtype;
+typedef enum { POLAR_SUM = 0, POLAR_MAX = 2, POLAR_MIN = 3 } polar_op;
+
+/* Collective / algorithm / protocol enums: SPEC.md L306 numbering
+ * (TREE=0, RING=1, NVLS=2; LL=0, LL128=1, SIMPLE=2) plus the two direct
+ * all-to-all algorithms this library adds. */
+enum { POLAR_COLL_ALLREDUCE = 0, POLAR_COLL_ALLGATHER = 1, POLAR_COLL_BROADCAST = 2,
+       POLAR_COLL_REDUCESCATTER = 3 };
+enum { POLAR_ALGO_TREE = 0, POLAR_ALGO_RING = 1, POLAR_ALGO_NVLS = 2 /* reserved */,
+       POLAR_ALGO_ONESHOT = 3, POLAR_ALGO_TWOSHOT = 4 };
+enum { POLAR_PROTO_LL = 0, POLAR_PROTO_LL128 = 1 /* reserved */, POLAR_PROTO_SIMPLE = 2 };
+
+#define POLAR_UNSET 0xFFFFFFFFu   /* algo/proto "defer to default"   */
+#define POLAR_MAXCH 32            /* channel clamp bound (R8) */
+#define POLAR_MAXRANKS 8          /* one NVLink node                                 */
+#define POLAR_MAXROWS 64          /* bounded policy table                            */
+
+/* ---------------------------------------------------------------- structs */
+
+/* Tuner context ("collective type, message size, rank count"). 16 B. */
+typedef struct {
+    uint32_t coll;     /* POLAR_COLL_*                                     */
+    uint32_t nranks;   /* participating ranks, 1..POLAR_MAXRANKS          */
+    uint64_t bytes;    /* total message bytes = count * element size      */
+} polar_ctx;
+
+/* Tuner outputs ("writes algorithm, protocol, and channel count")
+ * plus the policy generation that produced them. 16 B. */
+typedef struct {
+    uint32_t algo;        /* POLAR_ALGO_*                      */
+    uint32_t proto;       /* POLAR_PROTO_*                     */
+    uint32_t nchannels;   /* 1..POLAR_MAXCH                    */
+    uint32_t generation;  /* active policy generation at decide */
+} polar_decision;
+
+/* One policy row. 32 B.  A policy is an ordered list of rows; the first row with
+ * coll == ctx.coll, nranks in {0 (any), ctx.nranks} and ctx.bytes <= max_bytes
+ * (inclusive, "msg_size <= 32*1024") wins.  algo/proto may be
+ * POLAR_UNSET and nchannels 0 to defer that field to the built-in default
+ * (SPEC.md L339); nchannels is clamped to [1, POLAR_MAXCH]. */
+typedef struct {
+    uint32_t coll;
+    uint32_t nranks;      /* 0 = any                                */
+    uint64_t max_bytes;   /* inclusive upper bound on message bytes */
+    uint32_t algo;        /* POLAR_ALGO_* or POLAR_UNSET            */
+    uint32_t proto;       /* POLAR_PROTO_* or POLAR_UNSET           */
+    uint32_t nchannels;   /* 0 = UNSET; any other u32 is clamped    */
+    uint32_t _pad;        /* must be 0                              */
+} polar_policy_row;
+
+/* Host all-gather used ONLY at comm init / registration: gathers bytes_per_rank
+ * from every rank into recv (rank order).  Return 0 on success. */
+typedef int (*polar_allgather_fn)(const void* send, void* recv, size_t bytes_per_rank, void* user);
+
+typedef struct polar_comm_s* polar_comm_t;   /* opaque; owned by the library */
+
+/* ------------------------------------------------------ policy (decision hook) */
+
+/* Atomically replace the process-global policy (§4 "atomic
+ * compare-and-swap on the pointer").  The rows are COPIED.
+ * Validation: nrows <= 64; known enums; nranks <= 8; _pad == 0; rows of one
+ * (coll, nranks) group strictly ascending in max_bytes -> else POLAR_EINVAL;
+ * NVLS or LL128 -> POLAR_EUNSUPPORTED.  On any rejection the active policy and
+ * its generation are unchanged ("the old policy continues").
+ * nrows == 0 installs the empty policy (the paper's `noop`, L433).
+ * On success the generation increases by exactly 1 and is stored in
+ * *generation_out (may be NULL).  Retired tables stay allocated until process
+ * exit, so in-flight polar_decide calls never read freed memory (drain safety). */
+polar_status polar_set_policy(const polar_policy_row* rows, uint32_t nrows, uint32_t* generation_out);
+
+/* The decision hook: pure, wait-free (one acquire load + a <=64-row scan), any
+ * thread.  UNSET fields defer to the built-in default table (DESIGN.md "Default
+ * table"); nchannels clamped to [1, POLAR_MAXCH].  coll != ALLREDUCE ->
+ * POLAR_EUNSUPPORTED; NULL pointers or nranks outside 1..8 -> POLAR_EINVAL. */
+polar_status polar_decide(const polar_ctx* ctx, polar_decision* out);
+
+/* Batched form for sweeps/tests: out[i] = decide(ctx[i]); stops at the first error. */
+polar_status polar_decide_batch(const polar_ctx* ctx, polar_decision* out, size_t n);
+
+/* Active generation (0 before the first successful polar_set_policy). */
+uint32_t polar_policy_generation(void);
+
+/* Copy out the active rows (cap entries at most) and generation. */
+polar_status polar_get_policy(polar_policy_row* rows, uint32_t cap, uint32_t* nrows, uint32_t* generation);
+
+/* ------------------------------------------------------- decision-cost bench */
+
+typedef struct {
+    uint64_t calls;             /* timed calls                                   */
+    double p50_ns, p99_ns;      /* per-call, raw (timer pair included)           */
+    double mean_ns, min_ns, max_ns;
+    double timer_overhead_ns;   /* p50 of an empty timer pair                    */
+    double batched_mean_ns;     /* total / calls of an untimed-per-call loop      */
+} polar_bench_stats;
+
+/* BASELINE.json config 5 (SPEC.md L477-481 method): nwarm untimed warm-up calls,
+ * then ncalls calls each timed with a monotonic clock into a full sample buffer
+ * (samples_ns may be NULL; else ncalls entries), cycling through ctxs[0..nctx). */
+polar_status polar_bench_decide(const polar_ctx* ctxs, uint32_t nctx, uint64_t nwarm, uint64_t ncalls,
+                                uint64_t* samples_ns, polar_bench_stats* out);
+
+typedef struct {
+    uint64_t calls;             /* decisions returned (must equal issued)        */
+    uint64_t issued;            /* decisions requested                           */
+    uint64_t invalid;           /* decisions not produced by their generation's table */
+    uint64_t nonmonotonic;      /* per-thread generation decreases               */
+    uint64_t swaps;             /* successful swaps                              */
+    uint64_t rejected;          /* rejected (invalid-table) reload attempts      */
+    uint64_t rejected_changed;  /* rejections that changed the generation (must be 0) */
+    double swap_p50_ns, swap_p99_ns, swap_max_ns;   /* duration of the pointer swap */
+    uint32_t final_generation;
+} polar_swap_stats;
+
+/* SPEC.md L444-446 zero-loss stress: nthreads invokers issue calls_per_thread
+ * decisions each while one reloader alternates tables A and B nswaps times and,
+ * every 10th swap, attempts an invalid table that must be rejected.  Leaves
+ * the last installed table active. */
+polar_status polar_bench_swap(uint32_t nthreads, uint64_t calls_per_thread, uint32_t nswaps,
+                              const polar_policy_row* a, uint32_t na,
+                              const polar_policy_row* b, uint32_t nb,
+                              polar_swap_stats* out);
+
+/* ------------------------------------------------------------ communicators */
+
+/* Real multi-process comm: one rank per process, one GPU per rank (SURVEY.md
+ * §3(4)).  Allocates this rank's symmetric scratch (flags + staging) on
+ * cuda_device, exchanges CUDA IPC handles through `ag` (the only host
+ * collective), maps every peer's scratch and runs a device handshake.
+ * Collective.  nranks 1..8, 0 <= rank < nranks. */
+polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_device,
+                             polar_allgather_fn ag, void* user);
+
+/* Virtual comm: nranks logical ranks hosted by THIS process on ONE device; one
+ * kernel launch runs every rank's CTAs (grid = nranks x nchannels, a cooperative
+ * launch so that cross-rank waits cannot deadlock).  Same kernels, same
+ * protocols; peers are local HBM instead of NVLink. */
+polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device);
+
+polar_status polar_comm_destroy(polar_comm_t comm);   /* collective for real comms */
+
+/* nranks, this process's first rank, and how many ranks this process hosts
+ * (1 for a real comm, nranks for a virtual one).  Any out pointer may be NULL. */
+polar_status polar_comm_info(polar_comm_t comm, int* nranks, int* rank, int* nlocal);
+
+/* Symmetric allocation (collective): `bytes` of device memory per local rank,
+ * peer-mapped on every rank, so AllReduce on it is zero-copy.  ptrs receives
+ * nlocal device pointers.  Freed by polar_mem_free (collective) or destroy. */
+polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs);
+polar_status polar_mem_free(polar_comm_t comm, void* ptr);
+
+/* Register caller-owned device memory [buf, buf+bytes) for zero-copy use
+ * (collective; every rank registers its own buffer in the same call order).
+ * Virtual comms accept and ignore it (all ranks are local). */
+polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes);
+
+/* ----------------------------------------------------------------- AllReduce */
+
+/* In-place AllReduce of `count` elements at device pointer `buf` (real comm,
+ * nlocal == 1).  Decides (hook above), then launches ONE kernel on `stream`.
+ * count == 0 or nranks == 1 -> POLAR_OK without a launch.  buf need not be
+ * 16-B aligned (a scalar path is used) nor registered (two-shot then bounces
+ * through the symmetric scratch).  NULL buf with count > 0, bad dtype/op ->
+ * POLAR_EINVAL.  Result: every rank holds the rank-ordered reduction
+ * (SURVEY.md §8(c)), bitwise identical on every rank. */
+polar_status polar_allreduce(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype,
+                             polar_op op, void* stream);
+
+/* Same, for any comm: bufs[nlocal] device pointers, one per local rank
+ * (virtual comms: rank r's buffer is bufs[r]). */
+polar_status polar_allreduce_v(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype,
+                               polar_op op, void* stream);
+
+/* Same, but the decision is forced (sweeps, BASELINE config 3); `forced`'s
+ * algo/proto must be concrete, nchannels is clamped; generation is ignored. */
+polar_status polar_allreduce_forced(polar_comm_t comm, void* const* bufs, size_t count,
+                                    polar_dtype dtype, polar_op op, const polar_decision* forced,
+                                    void* stream);
+
+/* End-to-end form over HOST memory: host_bufs[nlocal] (pinned or pageable) are
+ * copied to the device buffers dev_bufs[nlocal], reduced in place, and the
+ * result is copied back into host_bufs; synchronous (returns after the D2H
+ * copy completed).  Used for the bench's e2e number. */
+polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, void* const* dev_bufs,
+                                  size_t count, polar_dtype dtype, polar_op op, void* stream);
+
+/* Decision used by the most recent AllReduce on this comm. */
+polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);
+
+/* Number of kernels this comm has launched so far (evidence for bench.py). */
+uint64_t polar_comm_launches(polar_comm_t comm);
+
+/* Latched asynchronous errors (device timeouts); POLAR_OK if none.  Does not
+ * synchronise: a timeout becomes visible once the kernel that hit it ended. */
+polar_status polar_comm_check(polar_comm_t comm);
+
+const char* polar_status_string(polar_status s);
+
+/* Library build tag, e.g. "polar 0.1 sm_100a". */
+const char* polar_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLAR_H */

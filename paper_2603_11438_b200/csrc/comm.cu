@@ -1,0 +1,529 @@
+// Communicators, symmetric memory, dispatch (include/polar.h).
+//
+// polar_allreduce: validate -> polar_decide (the tuner hook)
+// -> pick the kernel instance <dtype, op, algo, proto> -> ONE launch of
+// nlocal x nchannels CTAs on the caller's stream.  No host sync, no per-call
+// allocation.  Real comms map every peer's scratch with CUDA IPC (the only
+// host collective is the init/registration all-gather); virtual comms host all
+// ranks on one device and use a cooperative launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "device.cuh"
+#include "dispatch.h"
+#include "polar.h"
+#include "polar_internal.h"
+
+namespace polar {
+
+namespace dev {
+// init barrier: CTA b (local rank) signals every peer and waits for all
+__global__ void init_barrier_kernel(Params P, unsigned long long value) {
+    const int r = P.rank0 + (int)blockIdx.x;
+    const int tid = (int)threadIdx.x;
+    if (tid < P.nranks) st_release_sys(flag_ptr(P, tid, F_INIT, 0, r), value);
+    bool ok = true;
+    if (tid < P.nranks) ok = wait_geq(P, flag_ptr(P, r, F_INIT, 0, tid), value);
+    __syncthreads_and(ok);
+}
+}  // namespace dev
+
+const void* init_barrier_kernel_ptr() { return reinterpret_cast<const void*>(&dev::init_barrier_kernel); }
+
+static size_t env_size(const char* name, size_t dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    char* end = nullptr;
+    unsigned long long x = std::strtoull(v, &end, 0);
+    return x ? (size_t)x : dflt;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout make_layout(bool with_bounce) {
+    Layout L{};
+    size_t off = 0;
+    L.flags_off = off; off = align_up(off + kFlagBytes, 4096);
+    L.state_off = off; off = align_up(off + kStateBytes, 4096);
+    L.os_chunk = align_up(env_size("POLAR_OS_CHUNK", 1 << 20), 512);
+    L.os_off = off; off = align_up(off + 2 * kMaxRanks * L.os_chunk, 4096);
+    L.osll_chunk = align_up(env_size("POLAR_OSLL_CHUNK", 256 << 10), 512);
+    L.osll_off = off; off = align_up(off + 2 * kMaxRanks * 2 * L.osll_chunk, 4096);
+    L.tsll_chunk = align_up(env_size("POLAR_TSLL_CHUNK", 64 << 10), 512);
+    L.tsll_off = off; off = align_up(off + 2 * (2 * kMaxRanks * 2 * L.tsll_chunk), 4096);
+    L.ring_slot = align_up(env_size("POLAR_RING_SLOT", 128 << 10), 512);
+    L.ring_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring_slot, 4096);
+    L.ringll_slot = align_up(env_size("POLAR_RINGLL_SLOT", 64 << 10), 512);
+    L.ringll_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ringll_slot, 4096);
+    L.tree_slot = align_up(env_size("POLAR_TREE_SLOT", 128 << 10), 512);
+    L.tree_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.tree_slot, 4096);
+    L.treell_slot = align_up(env_size("POLAR_TREELL_SLOT", 64 << 10), 512);
+    L.treell_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.treell_slot, 4096);
+    L.bounce_bytes = with_bounce ? align_up(env_size("POLAR_BOUNCE", 64 << 20), 4096) : 0;
+    L.bounce_off = off; off = align_up(off + L.bounce_bytes, 4096);
+    L.total = off;
+    return L;
+}
+
+}  // namespace polar
+
+using namespace polar;
+
+struct Registration {
+    char* base;            // local device pointer
+    size_t bytes;
+    char* peer[kMaxRanks]; // rank p's registered base as mapped here
+    bool owned;            // allocated by polar_mem_alloc
+};
+
+struct polar_comm_s {
+    int nranks = 0, rank0 = 0, nlocal = 0, device = 0;
+    bool is_virtual = false;
+    Layout L{};
+    char* scratch_own[kMaxRanks] = {};   // allocations owned by this process
+    char* scratch[kMaxRanks] = {};       // rank p's scratch as addressable here
+    std::vector<Registration> regs;
+    std::vector<char*> ipc_mapped;       // to close at destroy
+    std::vector<char*> virt_allocs;      // polar_mem_alloc on virtual comms
+    int* err_host = nullptr;
+    int* err_dev = nullptr;
+    polar_decision last{};
+    uint64_t launches = 0;
+    polar_status latched = POLAR_OK;
+    polar_allgather_fn ag = nullptr;
+    void* user = nullptr;
+    uint64_t init_value = 0;
+    int max_coop_blocks = 0;             // virtual: co-residency bound
+    unsigned long long timeout_ns = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+inline polar_status cuerr(cudaError_t e) { return e == cudaSuccess ? POLAR_OK : POLAR_ECUDA; }
+
+#define CU_TRY(x)                                   \
+    do {                                            \
+        cudaError_t _e = (x);                       \
+        if (_e != cudaSuccess) return POLAR_ECUDA;  \
+    } while (0)
+
+int esize_of(int dtype) {
+    switch (dtype) {
+        case POLAR_INT32: case POLAR_FLOAT32: return 4;
+        case POLAR_INT64: return 8;
+        case POLAR_BFLOAT16: return 2;
+    }
+    return 0;
+}
+
+bool op_ok(int op) { return op == POLAR_SUM || op == POLAR_MAX || op == POLAR_MIN; }
+
+void fill_params(const polar_comm_s* c, dev::Params& P) {
+    std::memset(&P, 0, sizeof(P));
+    for (int p = 0; p < c->nranks; ++p) P.scratch[p] = c->scratch[p];
+    P.nranks = c->nranks;
+    P.rank0 = c->rank0;
+    P.err = c->err_dev;
+    P.timeout_ns = c->timeout_ns;
+    const Layout& L = c->L;
+    P.flags_off = L.flags_off; P.state_off = L.state_off;
+    P.os_off = L.os_off; P.os_chunk = L.os_chunk;
+    P.osll_off = L.osll_off; P.osll_chunk = L.osll_chunk;
+    P.tsll_off = L.tsll_off; P.tsll_chunk = L.tsll_chunk;
+    P.ring_off = L.ring_off; P.ring_slot = L.ring_slot;
+    P.ringll_off = L.ringll_off; P.ringll_slot = L.ringll_slot;
+    P.tree_off = L.tree_off; P.tree_slot = L.tree_slot;
+    P.treell_off = L.treell_off; P.treell_slot = L.treell_slot;
+}
+
+polar_status check_latched(polar_comm_s* c) {
+    if (c->latched != POLAR_OK) return c->latched;
+    int e = *(volatile int*)c->err_host;
+    if (e != 0) c->latched = (polar_status)e;
+    return c->latched;
+}
+
+polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int grid, cudaStream_t stream) {
+    void* args[] = {&P};
+    cudaError_t e;
+    if (c->is_virtual) {
+        e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(dev::kBlock), args, 0, stream);
+    } else {
+        e = cudaLaunchKernel(fn, dim3(grid), dim3(dev::kBlock), args, 0, stream);
+    }
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return POLAR_ECUDA;
+    }
+    c->launches++;
+    return POLAR_OK;
+}
+
+polar_status init_barrier(polar_comm_s* c) {
+    dev::Params P;
+    fill_params(c, P);
+    P.nch = 1;
+    c->init_value++;
+    void* args[] = {&P, &c->init_value};
+    cudaError_t e;
+    if (c->is_virtual)
+        e = cudaLaunchCooperativeKernel(init_barrier_kernel_ptr(), dim3(c->nlocal), dim3(dev::kBlock), args, 0, 0);
+    else
+        e = cudaLaunchKernel(init_barrier_kernel_ptr(), dim3(1), dim3(dev::kBlock), args, 0, 0);
+    if (e != cudaSuccess) return POLAR_ECUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return POLAR_ECUDA;
+    return check_latched(c);
+}
+
+polar_status alloc_common(polar_comm_s* c) {
+    c->timeout_ns = (unsigned long long)env_size("POLAR_TIMEOUT_MS", 20000) * 1000000ull;
+    CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
+    *c->err_host = 0;
+    CU_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+    return POLAR_OK;
+}
+
+// find a registration containing [p, p+bytes)
+const Registration* find_reg(const polar_comm_s* c, const char* p, size_t bytes) {
+    for (const auto& r : c->regs)
+        if (p >= r.base && p + bytes <= r.base + r.bytes) return &r;
+    return nullptr;
+}
+
+void destroy_comm(polar_comm_s* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (char* m : c->ipc_mapped) cudaIpcCloseMemHandle(m);
+    for (auto& r : c->regs)
+        if (r.owned) cudaFree(r.base);
+    for (char* v : c->virt_allocs) cudaFree(v);
+    for (int p = 0; p < kMaxRanks; ++p)
+        if (c->scratch_own[p]) cudaFree(c->scratch_own[p]);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    delete c;
+}
+
+// Exchange IPC handles of `base` (allocation start) + offset; fill peer[] pointers.
+polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks]) {
+    struct Msg { cudaIpcMemHandle_t h; unsigned long long off; int pid_ok; };
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    // cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link)
+    static CUresult (*getrange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+    if (!getrange) {
+        cudaDriverEntryPointQueryResult q;
+        void* fp = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess || !fp)
+            return POLAR_ECUDA;
+        getrange = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fp);
+    }
+    if (getrange(&base, &sz, (CUdeviceptr)ptr) != CUDA_SUCCESS) return POLAR_EINVAL;
+    Msg mine{};
+    CU_TRY(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)));
+    mine.off = (unsigned long long)(ptr - reinterpret_cast<char*>(base));
+    mine.pid_ok = 1;
+    std::vector<Msg> all(c->nranks);
+    if (c->ag(&mine, all.data(), sizeof(Msg), c->user) != 0) return POLAR_ESTATE;
+    for (int p = 0; p < c->nranks; ++p) {
+        if (p == c->rank0) { peer[p] = ptr; continue; }
+        void* m = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&m, all[p].h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) { (void)cudaGetLastError(); return POLAR_ECUDA; }
+        c->ipc_mapped.push_back(reinterpret_cast<char*>(m));
+        peer[p] = reinterpret_cast<char*>(m) + all[p].off;
+    }
+    return POLAR_OK;
+}
+
+polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int dtype, int op,
+                          const polar_decision* forced, cudaStream_t stream) {
+    const int es = esize_of(dtype);
+    if (!es || !op_ok(op)) return POLAR_EINVAL;
+    if (count > 0 && !bufs) return POLAR_EINVAL;
+    for (int l = 0; l < c->nlocal && count > 0; ++l)
+        if (!bufs[l] || (reinterpret_cast<uintptr_t>(bufs[l]) % es) != 0) return POLAR_EINVAL;
+    polar_status st = check_latched(c);
+    if (st != POLAR_OK) return st;
+    // --- decide (the tuner hook)
+    polar_decision d;
+    polar_ctx ctx{POLAR_COLL_ALLREDUCE, (uint32_t)c->nranks, (uint64_t)count * (uint64_t)es};
+    if (forced) {
+        d = *forced;
+        if (d.nchannels < 1) d.nchannels = 1;
+        if (d.nchannels > POLAR_MAXCH) d.nchannels = POLAR_MAXCH;
+        d.generation = polar_policy_generation();
+    } else {
+        st = polar_decide(&ctx, &d);
+        if (st != POLAR_OK) return st;
+    }
+    const void* fn = kernel_for(dtype, op, (int)d.algo, (int)d.proto);
+    if (!fn) return POLAR_EUNSUPPORTED;
+    if (c->is_virtual) {
+        const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
+        if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
+    }
+    c->last = d;
+    if (count == 0 || c->nranks == 1) return POLAR_OK;
+    if (cudaSetDevice(c->device) != cudaSuccess) return POLAR_ECUDA;
+
+    dev::Params P;
+    fill_params(c, P);
+    P.nch = (int)d.nchannels;
+    const int grid = c->nlocal * P.nch;
+    const size_t bytes = count * (size_t)es;
+
+    if (c->is_virtual) {
+        bool vec = true;
+        for (int p = 0; p < c->nranks; ++p) {
+            P.bufs[p] = reinterpret_cast<char*>(bufs[p]);
+            vec = vec && (reinterpret_cast<uintptr_t>(bufs[p]) % 16 == 0);
+        }
+        P.vec = vec;
+        P.count = count;
+        return launch_kernel(c, fn, P, grid, stream);
+    }
+    char* mine = reinterpret_cast<char*>(bufs[0]);
+    if (d.algo != POLAR_ALGO_TWOSHOT || d.proto != POLAR_PROTO_SIMPLE) {
+        // only the local buffer is touched directly; peers go through scratch
+        P.bufs[c->rank0] = mine;
+        P.vec = reinterpret_cast<uintptr_t>(mine) % 16 == 0;
+        P.count = count;
+        return launch_kernel(c, fn, P, grid, stream);
+    }
+    // zero-copy two-shot needs every rank's buffer mapped
+    const Registration* reg = find_reg(c, mine, bytes);
+    if (reg) {
+        const size_t off = (size_t)(mine - reg->base);
+        bool vec = true;
+        for (int p = 0; p < c->nranks; ++p) {
+            P.bufs[p] = reg->peer[p] + off;
+            vec = vec && (reinterpret_cast<uintptr_t>(P.bufs[p]) % 16 == 0);
+        }
+        P.vec = vec;
+        P.count = count;
+        return launch_kernel(c, fn, P, grid, stream);
+    }
+    // unregistered: bounce through the symmetric scratch, chunk by chunk
+    const size_t chunk_elems = std::max<size_t>(1, (c->L.bounce_bytes / es) & ~(size_t)7);
+    for (int p = 0; p < c->nranks; ++p) P.bufs[p] = c->scratch[p] + c->L.bounce_off;
+    P.vec = 1;   // the bounce region is 16-B aligned on every rank
+    for (size_t done = 0; done < count; done += chunk_elems) {
+        const size_t n = std::min(chunk_elems, count - done);
+        char* src = mine + done * es;
+        CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, stream));
+        P.count = n;
+        st = launch_kernel(c, fn, P, grid, stream);
+        if (st != POLAR_OK) return st;
+        CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, stream));
+    }
+    return POLAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_device, polar_allgather_fn ag,
+                             void* user) {
+    if (!out || nranks < 1 || nranks > POLAR_MAXRANKS || rank < 0 || rank >= nranks || !ag) return POLAR_EINVAL;
+    *out = nullptr;
+    polar_comm_s* c = new (std::nothrow) polar_comm_s;
+    if (!c) return POLAR_ENOMEM;
+    c->nranks = nranks;
+    c->rank0 = rank;
+    c->nlocal = 1;
+    c->device = cuda_device;
+    c->ag = ag;
+    c->user = user;
+    c->L = make_layout(true);
+    polar_status st = cuerr(cudaSetDevice(cuda_device));
+    if (st == POLAR_OK) st = alloc_common(c);
+    if (st == POLAR_OK) st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[0]), c->L.total));
+    if (st == POLAR_OK) st = cuerr(cudaMemset(c->scratch_own[0], 0, c->L.total));
+    if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
+    if (st == POLAR_OK) st = exchange_and_map(c, c->scratch_own[0], c->scratch);
+    if (st == POLAR_OK) st = init_barrier(c);
+    if (st != POLAR_OK) { destroy_comm(c); return st; }
+    *out = c;
+    return POLAR_OK;
+}
+
+polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device) {
+    if (!out || nranks < 1 || nranks > POLAR_MAXRANKS) return POLAR_EINVAL;
+    *out = nullptr;
+    polar_comm_s* c = new (std::nothrow) polar_comm_s;
+    if (!c) return POLAR_ENOMEM;
+    c->nranks = nranks;
+    c->rank0 = 0;
+    c->nlocal = nranks;
+    c->device = cuda_device;
+    c->is_virtual = true;
+    c->L = make_layout(false);
+    polar_status st = cuerr(cudaSetDevice(cuda_device));
+    if (st == POLAR_OK) st = alloc_common(c);
+    for (int p = 0; p < nranks && st == POLAR_OK; ++p) {
+        st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[p]), c->L.total));
+        if (st == POLAR_OK) st = cuerr(cudaMemset(c->scratch_own[p], 0, c->L.total));
+        c->scratch[p] = c->scratch_own[p];
+    }
+    if (st == POLAR_OK) {
+        // co-residency bound for the cooperative launch (smallest over all kernels we may launch)
+        int sms = 0, per_sm = 0, minper = 1 << 30;
+        st = cuerr(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
+        const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
+        const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
+        const int algos[] = {POLAR_ALGO_TREE, POLAR_ALGO_RING, POLAR_ALGO_ONESHOT, POLAR_ALGO_TWOSHOT};
+        const int protos[] = {POLAR_PROTO_LL, POLAR_PROTO_SIMPLE};
+        for (int dt : dts) for (int op : ops) for (int a : algos) for (int pr : protos) {
+            if (st != POLAR_OK) break;
+            const void* fn = kernel_for(dt, op, a, pr);
+            st = cuerr(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kBlock, 0));
+            minper = std::min(minper, per_sm);
+        }
+        c->max_coop_blocks = sms * minper;
+        if (st == POLAR_OK && c->max_coop_blocks < nranks) st = POLAR_EUNSUPPORTED;
+    }
+    if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
+    if (st == POLAR_OK) st = init_barrier(c);
+    if (st != POLAR_OK) { destroy_comm(c); return st; }
+    *out = c;
+    return POLAR_OK;
+}
+
+polar_status polar_comm_destroy(polar_comm_t comm) {
+    if (!comm) return POLAR_EINVAL;
+    destroy_comm(comm);
+    return POLAR_OK;
+}
+
+polar_status polar_comm_info(polar_comm_t comm, int* nranks, int* rank, int* nlocal) {
+    if (!comm) return POLAR_EINVAL;
+    if (nranks) *nranks = comm->nranks;
+    if (rank) *rank = comm->rank0;
+    if (nlocal) *nlocal = comm->nlocal;
+    return POLAR_OK;
+}
+
+polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs) {
+    if (!comm || !ptrs || bytes == 0) return POLAR_EINVAL;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    CU_TRY(cudaSetDevice(comm->device));
+    if (comm->is_virtual) {
+        for (int p = 0; p < comm->nranks; ++p) {
+            char* m = nullptr;
+            if (cudaMalloc(reinterpret_cast<void**>(&m), bytes) != cudaSuccess) return POLAR_ENOMEM;
+            comm->virt_allocs.push_back(m);
+            ptrs[p] = m;
+        }
+        return POLAR_OK;
+    }
+    Registration r{};
+    if (cudaMalloc(reinterpret_cast<void**>(&r.base), bytes) != cudaSuccess) return POLAR_ENOMEM;
+    r.bytes = bytes;
+    r.owned = true;
+    polar_status st = exchange_and_map(comm, r.base, r.peer);
+    if (st != POLAR_OK) { cudaFree(r.base); return st; }
+    comm->regs.push_back(r);
+    ptrs[0] = r.base;
+    return POLAR_OK;
+}
+
+polar_status polar_mem_free(polar_comm_t comm, void* ptr) {
+    if (!comm || !ptr) return POLAR_EINVAL;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    cudaSetDevice(comm->device);
+    cudaDeviceSynchronize();
+    for (size_t i = 0; i < comm->virt_allocs.size(); ++i)
+        if (comm->virt_allocs[i] == ptr) {
+            cudaFree(ptr);
+            comm->virt_allocs.erase(comm->virt_allocs.begin() + (long)i);
+            return POLAR_OK;
+        }
+    for (size_t i = 0; i < comm->regs.size(); ++i)
+        if (comm->regs[i].base == ptr && comm->regs[i].owned) {
+            // peers' mappings of this buffer stay open until destroy (IPC handles are per allocation)
+            cudaFree(ptr);
+            comm->regs.erase(comm->regs.begin() + (long)i);
+            return POLAR_OK;
+        }
+    return POLAR_EINVAL;
+}
+
+polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes) {
+    if (!comm || !buf || bytes == 0) return POLAR_EINVAL;
+    if (comm->is_virtual) return POLAR_OK;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    CU_TRY(cudaSetDevice(comm->device));
+    Registration r{};
+    r.base = reinterpret_cast<char*>(buf);
+    r.bytes = bytes;
+    r.owned = false;
+    polar_status st = exchange_and_map(comm, r.base, r.peer);
+    if (st != POLAR_OK) return st;
+    comm->regs.push_back(r);
+    return POLAR_OK;
+}
+
+polar_status polar_allreduce(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, polar_op op,
+                             void* stream) {
+    if (!comm) return POLAR_EINVAL;
+    if (comm->nlocal != 1) return POLAR_EINVAL;
+    void* bufs[1] = {buf};
+    return do_allreduce(comm, bufs, count, dtype, op, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_allreduce_v(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype, polar_op op,
+                               void* stream) {
+    if (!comm) return POLAR_EINVAL;
+    return do_allreduce(comm, bufs, count, dtype, op, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_allreduce_forced(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype,
+                                    polar_op op, const polar_decision* forced, void* stream) {
+    if (!comm || !forced) return POLAR_EINVAL;
+    return do_allreduce(comm, bufs, count, dtype, op, forced, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, void* const* dev_bufs, size_t count,
+                                  polar_dtype dtype, polar_op op, void* stream) {
+    if (!comm || (count && (!host_bufs || !dev_bufs))) return POLAR_EINVAL;
+    const int es = esize_of(dtype);
+    if (!es) return POLAR_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    CU_TRY(cudaSetDevice(comm->device));
+    const size_t bytes = count * (size_t)es;
+    for (int l = 0; l < comm->nlocal && count; ++l)
+        CU_TRY(cudaMemcpyAsync(dev_bufs[l], host_bufs[l], bytes, cudaMemcpyHostToDevice, s));
+    polar_status st = do_allreduce(comm, dev_bufs, count, dtype, op, nullptr, s);
+    if (st != POLAR_OK) return st;
+    for (int l = 0; l < comm->nlocal && count; ++l)
+        CU_TRY(cudaMemcpyAsync(host_bufs[l], dev_bufs[l], bytes, cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    return check_latched(comm);
+}
+
+polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out) {
+    if (!comm || !out) return POLAR_EINVAL;
+    *out = comm->last;
+    return POLAR_OK;
+}
+
+uint64_t polar_comm_launches(polar_comm_t comm) { return comm ? comm->launches : 0; }
+
+polar_status polar_comm_check(polar_comm_t comm) {
+    if (!comm) return POLAR_EINVAL;
+    return check_latched(comm);
+}
+
+const char* polar_version(void) { return "polar 0.1 sm_100a"; }
+
+}  // extern "C"

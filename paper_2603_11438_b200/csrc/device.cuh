@@ -1,0 +1,292 @@
+// Device primitives for the polar kernels (sm_100a): cross-rank flags, LL lines,
+// 16-byte packs with partial tails, and the reduction arithmetic (SURVEY.md §8(a)
+// rows a7, a8, a10, a11).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "polar.h"
+#include "polar_internal.h"
+
+namespace polar {
+namespace dev {
+
+// ------------------------------------------------------------- kernel params
+
+constexpr int kBlock = 512;   // threads per CTA (one CTA per rank-channel)
+
+struct Params {
+    char* bufs[kMaxRanks];     // rank p's data for this call (peer-mapped; zero-copy two-shot uses all)
+    char* scratch[kMaxRanks];  // rank p's scratch base (peer-mapped)
+    unsigned long long count;  // elements
+    int nranks;                // ranks in the comm
+    int rank0;                 // first rank hosted by this launch
+    int nch;                   // channels (CTAs per rank)
+    int vec;                   // 1: every buffer of this call is 16-B aligned
+    int* err;                  // host-mapped error word (first error wins)
+    unsigned long long timeout_ns;
+    // layout (identical on every rank)
+    unsigned long long flags_off, state_off;
+    unsigned long long os_off, os_chunk, osll_off, osll_chunk, tsll_off, tsll_chunk;
+    unsigned long long ring_off, ring_slot, ringll_off, ringll_slot;
+    unsigned long long tree_off, tree_slot, treell_off, treell_slot;
+};
+
+// -------------------------------------------------------------- raw memory ops
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// data loads that must not hit a stale L1 line (peer data, staging reused within a kernel)
+__device__ __forceinline__ uint4 ld_cg(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_plain(uint4* p, uint4 v) { *p = v; }
+
+// LL line: 16 B = {d0, flag, d1, flag}; written with one 16-B volatile store,
+// polled with one 16-B volatile load.
+__device__ __forceinline__ void st_ll(uint4* p, uint32_t d0, uint32_t d1, uint32_t flag) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(d0), "r"(flag), "r"(d1),
+                 "r"(flag)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+// ------------------------------------------------------------------ errors
+
+__device__ __forceinline__ void raise_error(const Params& P, int code) {
+    // host-mapped word; plain store (no PCIe atomics needed): every writer stores a nonzero code
+    *(volatile int*)P.err = code;
+    __threadfence_system();
+}
+
+// Spin until *p >= v; false on timeout (error latched).
+static __device__ __noinline__ bool wait_geq(const Params& P, const uint64_t* p, uint64_t v) {
+    if (ld_acquire_sys(p) >= v) return true;
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1;; ++it) {
+        if (ld_acquire_sys(p) >= v) return true;
+        if ((it & 255) == 0) {
+            if (globaltimer() - t0 > P.timeout_ns) {
+                raise_error(P, POLAR_ETIMEOUT);
+                return false;
+            }
+            if (*(volatile int*)P.err) return false;   // someone else failed: give up too
+        }
+    }
+}
+
+// Poll one LL line until both flags equal `flag`; false on timeout.
+__device__ __forceinline__ bool poll_ll(const Params& P, const uint4* p, uint32_t flag, uint4& out) {
+    uint4 v = ld_ll(p);
+    if (v.y == flag && v.w == flag) { out = v; return true; }
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1;; ++it) {
+        v = ld_ll(p);
+        if (v.y == flag && v.w == flag) { out = v; return true; }
+        if ((it & 1023) == 0) {
+            if (globaltimer() - t0 > P.timeout_ns) {
+                raise_error(P, POLAR_ETIMEOUT);
+                return false;
+            }
+            if (*(volatile int*)P.err) return false;
+        }
+    }
+}
+
+// ------------------------------------------------------------ scratch access
+
+__device__ __forceinline__ uint64_t* flag_ptr(const Params& P, int owner, int kind, int ch, int slot) {
+    return reinterpret_cast<uint64_t*>(P.scratch[owner] + P.flags_off + ((size_t)kind * kMaxCh + ch) * kFlagRow) +
+           slot;
+}
+__device__ __forceinline__ ChanState* chan_state(const Params& P, int rank, int ch) {
+    return reinterpret_cast<ChanState*>(P.scratch[rank] + P.state_off) + ch;
+}
+
+// ------------------------------------------------------------------ dtypes
+
+template <int DT> struct DType;
+template <> struct DType<POLAR_INT32> { using T = int32_t; static constexpr int ES = 4; };
+template <> struct DType<POLAR_INT64> { using T = long long; static constexpr int ES = 8; };
+template <> struct DType<POLAR_FLOAT32> { using T = float; static constexpr int ES = 4; };
+template <> struct DType<POLAR_BFLOAT16> { using T = __nv_bfloat16; static constexpr int ES = 2; };
+
+// Accumulator of one 16-B pack.  For bf16 it holds 8 f32 partials (32 B on the
+// wire: "bf16 reduce-phase partials travel as f32").
+template <int DT> struct Acc { uint4 w[1]; };
+template <> struct Acc<POLAR_BFLOAT16> { uint4 w[2]; };
+template <int DT> struct AccWords { static constexpr int N = 1; };
+template <> struct AccWords<POLAR_BFLOAT16> { static constexpr int N = 2; };
+
+__device__ __forceinline__ uint32_t u32_comb(uint32_t a, uint32_t b, int op) {
+    if (op == POLAR_SUM) return a + b;   // two's-complement wrap
+    int x = (int)a, y = (int)b;
+    return (uint32_t)(op == POLAR_MAX ? (x > y ? x : y) : (x < y ? x : y));
+}
+__device__ __forceinline__ unsigned long long u64_comb(unsigned long long a, unsigned long long b, int op) {
+    if (op == POLAR_SUM) return a + b;
+    long long x = (long long)a, y = (long long)b;
+    return (unsigned long long)(op == POLAR_MAX ? (x > y ? x : y) : (x < y ? x : y));
+}
+__device__ __forceinline__ float f32_comb(float a, float b, int op) {
+    if (op == POLAR_SUM) return __fadd_rn(a, b);   // one RNE add, never contracted
+    return op == POLAR_MAX ? fmaxf(a, b) : fminf(a, b);
+}
+__device__ __forceinline__ uint32_t f32_comb_bits(uint32_t a, uint32_t b, int op) {
+    return __float_as_uint(f32_comb(__uint_as_float(a), __uint_as_float(b), op));
+}
+
+// acc <- widen(pack)
+template <int DT> __device__ __forceinline__ void acc_init(Acc<DT>& a, uint4 p) {
+    if constexpr (DT == POLAR_BFLOAT16) {
+        a.w[0] = make_uint4(p.x << 16, p.x & 0xFFFF0000u, p.y << 16, p.y & 0xFFFF0000u);
+        a.w[1] = make_uint4(p.z << 16, p.z & 0xFFFF0000u, p.w << 16, p.w & 0xFFFF0000u);
+    } else {
+        a.w[0] = p;
+    }
+}
+
+// acc <- acc (op) widen(pack)
+template <int DT, int OP> __device__ __forceinline__ void acc_add(Acc<DT>& a, uint4 p) {
+    if constexpr (DT == POLAR_INT32) {
+        a.w[0].x = u32_comb(a.w[0].x, p.x, OP); a.w[0].y = u32_comb(a.w[0].y, p.y, OP);
+        a.w[0].z = u32_comb(a.w[0].z, p.z, OP); a.w[0].w = u32_comb(a.w[0].w, p.w, OP);
+    } else if constexpr (DT == POLAR_INT64) {
+        unsigned long long a0 = ((unsigned long long)a.w[0].y << 32) | a.w[0].x;
+        unsigned long long a1 = ((unsigned long long)a.w[0].w << 32) | a.w[0].z;
+        unsigned long long b0 = ((unsigned long long)p.y << 32) | p.x;
+        unsigned long long b1 = ((unsigned long long)p.w << 32) | p.z;
+        a0 = u64_comb(a0, b0, OP); a1 = u64_comb(a1, b1, OP);
+        a.w[0] = make_uint4((uint32_t)a0, (uint32_t)(a0 >> 32), (uint32_t)a1, (uint32_t)(a1 >> 32));
+    } else if constexpr (DT == POLAR_FLOAT32) {
+        a.w[0].x = f32_comb_bits(a.w[0].x, p.x, OP); a.w[0].y = f32_comb_bits(a.w[0].y, p.y, OP);
+        a.w[0].z = f32_comb_bits(a.w[0].z, p.z, OP); a.w[0].w = f32_comb_bits(a.w[0].w, p.w, OP);
+    } else {
+        Acc<DT> b;
+        acc_init<DT>(b, p);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            a.w[k].x = f32_comb_bits(a.w[k].x, b.w[k].x, OP); a.w[k].y = f32_comb_bits(a.w[k].y, b.w[k].y, OP);
+            a.w[k].z = f32_comb_bits(a.w[k].z, b.w[k].z, OP); a.w[k].w = f32_comb_bits(a.w[k].w, b.w[k].w, OP);
+        }
+    }
+}
+
+// acc <- acc (op) acc2 (both already widened; used when partials meet partials)
+template <int DT, int OP> __device__ __forceinline__ void acc_merge(Acc<DT>& a, const Acc<DT>& b) {
+    if constexpr (DT == POLAR_BFLOAT16) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            a.w[k].x = f32_comb_bits(a.w[k].x, b.w[k].x, OP); a.w[k].y = f32_comb_bits(a.w[k].y, b.w[k].y, OP);
+            a.w[k].z = f32_comb_bits(a.w[k].z, b.w[k].z, OP); a.w[k].w = f32_comb_bits(a.w[k].w, b.w[k].w, OP);
+        }
+    } else {
+        acc_add<DT, OP>(a, b.w[0]);
+    }
+}
+
+__device__ __forceinline__ uint32_t bf16x2_rn(uint32_t lo_f32, uint32_t hi_f32) {
+    __nv_bfloat16 l = __float2bfloat16_rn(__uint_as_float(lo_f32));
+    __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(hi_f32));
+    return (uint32_t)__bfloat16_as_ushort(l) | ((uint32_t)__bfloat16_as_ushort(h) << 16);
+}
+
+// pack <- narrow(acc): the single bf16 rounding (RNE) of every output element
+template <int DT> __device__ __forceinline__ uint4 acc_fin(const Acc<DT>& a) {
+    if constexpr (DT == POLAR_BFLOAT16) {
+        return make_uint4(bf16x2_rn(a.w[0].x, a.w[0].y), bf16x2_rn(a.w[0].z, a.w[0].w),
+                          bf16x2_rn(a.w[1].x, a.w[1].y), bf16x2_rn(a.w[1].z, a.w[1].w));
+    } else {
+        return a.w[0];
+    }
+}
+
+// ----------------------------------------------------- packs of user data
+// The message is a sequence of 16-B packs; the last one may be partial
+// (nvalid < 16/ES elements).  Unaligned buffers fall back to element copies.
+
+template <int ES> __device__ __forceinline__ int pack_valid(unsigned long long count, unsigned long long idx) {
+    constexpr unsigned long long V = 16 / ES;
+    unsigned long long rem = count - idx * V;
+    return rem >= V ? (int)V : (int)rem;
+}
+
+template <int ES> __device__ __forceinline__ uint4 load_pack_slow(const char* base, unsigned long long idx, int nvalid) {
+    uint4 r = make_uint4(0, 0, 0, 0);
+    char* rb = reinterpret_cast<char*>(&r);
+    const char* src = base + idx * 16;
+    for (int i = 0; i < nvalid; ++i) {
+        if constexpr (ES == 2) reinterpret_cast<uint16_t*>(rb)[i] = reinterpret_cast<const uint16_t*>(src)[i];
+        else if constexpr (ES == 4) reinterpret_cast<uint32_t*>(rb)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+        else reinterpret_cast<unsigned long long*>(rb)[i] = reinterpret_cast<const unsigned long long*>(src)[i];
+    }
+    return r;
+}
+template <int ES> __device__ __forceinline__ void store_pack_slow(char* base, unsigned long long idx, uint4 v, int nvalid) {
+    const char* vb = reinterpret_cast<const char*>(&v);
+    char* dst = base + idx * 16;
+    for (int i = 0; i < nvalid; ++i) {
+        if constexpr (ES == 2) reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(vb)[i];
+        else if constexpr (ES == 4) reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(vb)[i];
+        else reinterpret_cast<unsigned long long*>(dst)[i] = reinterpret_cast<const unsigned long long*>(vb)[i];
+    }
+}
+
+// load pack idx of a user buffer (own or peer); .cg keeps peer data out of L1
+template <int ES> __device__ __forceinline__ uint4 load_pack(const Params& P, const char* base, unsigned long long idx) {
+    int nv = pack_valid<ES>(P.count, idx);
+    if (P.vec && nv == 16 / ES) return ld_cg(reinterpret_cast<const uint4*>(base) + idx);
+    return load_pack_slow<ES>(base, idx, nv);
+}
+template <int ES> __device__ __forceinline__ void store_pack(const Params& P, char* base, unsigned long long idx, uint4 v) {
+    int nv = pack_valid<ES>(P.count, idx);
+    if (P.vec && nv == 16 / ES) { reinterpret_cast<uint4*>(base)[idx] = v; return; }
+    store_pack_slow<ES>(base, idx, v, nv);
+}
+
+// ------------------------------------------------------------ partitioning
+// Ranges of packs in 32-pack (512 B) units so that shards/slices start on 512 B.
+constexpr unsigned long long kUnit = 32;
+
+__device__ __forceinline__ void split_range(unsigned long long lo, unsigned long long hi, int parts, int k,
+                                            unsigned long long& a, unsigned long long& b) {
+    unsigned long long units = (hi - lo + kUnit - 1) / kUnit;
+    unsigned long long ua = units * (unsigned long long)k / (unsigned long long)parts;
+    unsigned long long ub = units * (unsigned long long)(k + 1) / (unsigned long long)parts;
+    a = lo + ua * kUnit;
+    b = lo + ub * kUnit;
+    if (a > hi) a = hi;
+    if (b > hi) b = hi;
+}
+
+}  // namespace dev
+}  // namespace polar

@@ -1,0 +1,32 @@
+// Kernel instantiations for dtype POLAR_BFLOAT16 (see dispatch.h).
+#include "dispatch.h"
+#include "kernels.cuh"
+
+namespace polar {
+
+template <int OP, int ALGO, int PROTO>
+static const void* k() { return reinterpret_cast<const void*>(&dev::allreduce_kernel<POLAR_BFLOAT16, OP, ALGO, PROTO>); }
+
+template <int OP>
+static const void* by_algo(int algo, int proto) {
+    const bool ll = proto == POLAR_PROTO_LL;
+    if (proto != POLAR_PROTO_LL && proto != POLAR_PROTO_SIMPLE) return nullptr;
+    switch (algo) {
+        case POLAR_ALGO_TWOSHOT: return ll ? k<OP, POLAR_ALGO_TWOSHOT, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE>();
+        case POLAR_ALGO_ONESHOT: return ll ? k<OP, POLAR_ALGO_ONESHOT, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE>();
+        case POLAR_ALGO_RING: return ll ? k<OP, POLAR_ALGO_RING, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_RING, POLAR_PROTO_SIMPLE>();
+        case POLAR_ALGO_TREE: return ll ? k<OP, POLAR_ALGO_TREE, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_TREE, POLAR_PROTO_SIMPLE>();
+    }
+    return nullptr;
+}
+
+const void* kernel_bf16(int op, int algo, int proto) {
+    switch (op) {
+        case POLAR_SUM: return by_algo<POLAR_SUM>(algo, proto);
+        case POLAR_MAX: return by_algo<POLAR_MAX>(algo, proto);
+        case POLAR_MIN: return by_algo<POLAR_MIN>(algo, proto);
+    }
+    return nullptr;
+}
+
+}  // namespace polar

@@ -1,0 +1,585 @@
+// The AllReduce kernels.
+//
+// One kernel per <dtype, op, algorithm, protocol>.  Grid = nlocal x nch CTAs:
+// block b serves rank rank0 + b / nch on channel c = b % nch (a real comm has
+// nlocal = 1; a virtual comm hosts every rank in one cooperative launch).
+// Every cross-rank exchange is a direct load/store on a peer-mapped pointer
+// (NVLink/NVSwitch on a real node), ordered by u64 flags or flag-in-data LL
+// lines; nothing goes through NCCL or the host.
+//
+// Reduction order (R2-R4):
+//   one-shot / two-shot : x_0 (op) x_1 (op) ... (op) x_{n-1}   == the oracle, bit for bit
+//   ring                : chunk k starts at rank k and follows the ring
+//   tree                : node = own (op) child0 (op) child1, root rotated per channel
+// bf16 accumulates in f32 everywhere and is rounded once per output element.
+#pragma once
+#include "device.cuh"
+
+namespace polar {
+namespace dev {
+
+struct Who {
+    int r, c, n, tid;
+};
+
+__device__ __forceinline__ Who who(const Params& P) {
+    Who w;
+    w.r = P.rank0 + (int)blockIdx.x / P.nch;
+    w.c = (int)blockIdx.x % P.nch;
+    w.n = P.nranks;
+    w.tid = (int)threadIdx.x;
+    return w;
+}
+
+template <int ES> __device__ __forceinline__ unsigned long long npacks(const Params& P) {
+    return (P.count + (16 / ES) - 1) / (16 / ES);
+}
+
+// ===================================================================== two-shot
+// Simple, zero-copy on symmetric buffers: entry barrier; owner r reads shard r
+// from every rank, reduces in rank order, stores the result into every rank's
+// shard r; exit barrier.  NVLink bytes per rank: 2(n-1)/n * S.
+
+template <int DT, int OP>
+__device__ void twoshot_simple(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    const int n = w.n, tid = w.tid;
+    ChanState* st = chan_state(P, w.r, w.c);
+    const uint64_t e = st->epoch + 1;
+    if (tid < n) st_release_sys(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e);
+    bool ok = true;
+    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
+    if (!__syncthreads_and(ok)) return;
+
+    const unsigned long long NP = npacks<ES>(P);
+    unsigned long long s0, s1, a, b;
+    split_range(0, NP, n, w.r, s0, s1);
+    split_range(s0, s1, P.nch, w.c, a, b);
+    for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+        uint4 v[kMaxRanks];
+#pragma unroll
+        for (int p = 0; p < kMaxRanks; ++p)
+            if (p < n) v[p] = load_pack<ES>(P, P.bufs[p], i);
+        Acc<DT> acc;
+        acc_init<DT>(acc, v[0]);
+#pragma unroll
+        for (int p = 1; p < kMaxRanks; ++p)
+            if (p < n) acc_add<DT, OP>(acc, v[p]);
+        const uint4 out = acc_fin<DT>(acc);
+#pragma unroll
+        for (int p = 0; p < kMaxRanks; ++p)
+            if (p < n) store_pack<ES>(P, P.bufs[p], i, out);
+    }
+    __syncthreads();
+    if (tid < n) {
+        fence_acq_rel_sys();
+        st_relaxed_sys(flag_ptr(P, tid, F_EXIT, w.c, w.r), e);
+    }
+    ok = true;
+    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
+    if (!__syncthreads_and(ok)) return;
+    if (tid == 0) st->epoch = e;
+}
+
+// Two-shot LL: push-based.  RS: rank r writes its part of owner j's shard as LL
+// lines into j's RS staging slot r; owner polls, reduces in rank order, writes
+// its own buffer and pushes the result as LL lines into every rank's AG slot;
+// every rank polls the AG slots.  Two NVLink hops, no separate flags.
+
+__device__ __forceinline__ uint4* tsll_rs(const Params& P, int owner, int par, int slot) {
+    return reinterpret_cast<uint4*>(P.scratch[owner] + P.tsll_off +
+                                    ((size_t)(par * kMaxRanks + slot)) * 2 * P.tsll_chunk);
+}
+__device__ __forceinline__ uint4* tsll_ag(const Params& P, int owner, int par, int slot) {
+    return reinterpret_cast<uint4*>(P.scratch[owner] + P.tsll_off + (size_t)2 * kMaxRanks * 2 * P.tsll_chunk +
+                                    ((size_t)(par * kMaxRanks + slot)) * 2 * P.tsll_chunk);
+}
+
+template <int DT, int OP>
+__device__ void twoshot_ll(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    const int n = w.n, tid = w.tid;
+    ChanState* st = chan_state(P, w.r, w.c);
+    const uint64_t e0 = st->epoch;
+    const unsigned long long NP = npacks<ES>(P);
+    const unsigned long long SC = P.tsll_chunk / 16;   // packs per owner per chunk
+    const unsigned long long CH = SC * (unsigned long long)n;
+    const unsigned long long nchunks = (NP + CH - 1) / CH;
+    char* mine = P.bufs[w.r];
+    bool ok = true;
+    for (unsigned long long k = 0; k < nchunks; ++k) {
+        const uint64_t e = e0 + k + 1;
+        const uint32_t f = (uint32_t)e;
+        const int par = (int)(e & 1);
+        const unsigned long long clo = k * CH;
+        // RS push: my contribution to every other owner's part
+        for (int j = 0; j < n && ok; ++j) {
+            if (j == w.r) continue;
+            unsigned long long plo = clo + SC * j, phi = plo + SC;
+            if (plo > NP) plo = NP;
+            if (phi > NP) phi = NP;
+            unsigned long long a, b;
+            split_range(plo, phi, P.nch, w.c, a, b);
+            uint4* dst = tsll_rs(P, j, par, w.r);
+            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+                uint4 v = load_pack<ES>(P, mine, i);
+                uint4* l = dst + 2 * (i - plo);
+                st_ll(l, v.x, v.y, f);
+                st_ll(l + 1, v.z, v.w, f);
+            }
+        }
+        // reduce my part, push result to every rank
+        {
+            unsigned long long plo = clo + SC * w.r, phi = plo + SC;
+            if (plo > NP) plo = NP;
+            if (phi > NP) phi = NP;
+            unsigned long long a, b;
+            split_range(plo, phi, P.nch, w.c, a, b);
+            for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
+                Acc<DT> acc;
+                for (int p = 0; p < n && ok; ++p) {
+                    uint4 v;
+                    if (p == w.r) {
+                        v = load_pack<ES>(P, mine, i);
+                    } else {
+                        const uint4* l = tsll_rs(P, w.r, par, p) + 2 * (i - plo);
+                        uint4 l0, l1;
+                        ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
+                        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+                    }
+                    if (p == 0) acc_init<DT>(acc, v);
+                    else acc_add<DT, OP>(acc, v);
+                }
+                if (!ok) break;
+                const uint4 out = acc_fin<DT>(acc);
+                store_pack<ES>(P, mine, i, out);
+                for (int p = 0; p < n; ++p) {
+                    if (p == w.r) continue;
+                    uint4* l = tsll_ag(P, p, par, w.r) + 2 * (i - plo);
+                    st_ll(l, out.x, out.y, f);
+                    st_ll(l + 1, out.z, out.w, f);
+                }
+            }
+        }
+        // AG receive: results of every other owner
+        for (int j = 0; j < n && ok; ++j) {
+            if (j == w.r) continue;
+            unsigned long long plo = clo + SC * j, phi = plo + SC;
+            if (plo > NP) plo = NP;
+            if (phi > NP) phi = NP;
+            unsigned long long a, b;
+            split_range(plo, phi, P.nch, w.c, a, b);
+            const uint4* src = tsll_ag(P, w.r, par, j);
+            for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
+                const uint4* l = src + 2 * (i - plo);
+                uint4 l0, l1;
+                ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
+                if (ok) store_pack<ES>(P, mine, i, make_uint4(l0.x, l0.z, l1.x, l1.z));
+            }
+        }
+        if (!__syncthreads_and(ok)) return;   // parity reuse safety
+    }
+    if (tid == 0) st->epoch = e0 + nchunks;
+}
+
+// ===================================================================== one-shot
+// Every rank pushes its slice to slot r of every peer's staging, then reduces
+// slots 0..n-1 in rank order into its own buffer.  One NVLink step;
+// egress (n-1)*S.  Chunked through 2 parities when S exceeds a staging slot.
+
+__device__ __forceinline__ uint4* os_slot(const Params& P, int owner, int par, int slot) {
+    return reinterpret_cast<uint4*>(P.scratch[owner] + P.os_off + ((size_t)(par * kMaxRanks + slot)) * P.os_chunk);
+}
+__device__ __forceinline__ uint4* osll_slot(const Params& P, int owner, int par, int slot) {
+    return reinterpret_cast<uint4*>(P.scratch[owner] + P.osll_off +
+                                    ((size_t)(par * kMaxRanks + slot)) * 2 * P.osll_chunk);
+}
+
+template <int DT, int OP>
+__device__ void oneshot_simple(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    const int n = w.n, tid = w.tid;
+    ChanState* st = chan_state(P, w.r, w.c);
+    const uint64_t e0 = st->epoch;
+    const unsigned long long NP = npacks<ES>(P);
+    const unsigned long long CP = P.os_chunk / 16;
+    const unsigned long long nchunks = (NP + CP - 1) / CP;
+    char* mine = P.bufs[w.r];
+    for (unsigned long long k = 0; k < nchunks; ++k) {
+        const uint64_t e = e0 + k + 1;
+        const int par = (int)(e & 1);
+        const unsigned long long lo = k * CP, hi = (lo + CP < NP) ? lo + CP : NP;
+        unsigned long long a, b;
+        split_range(lo, hi, P.nch, w.c, a, b);
+        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+            const uint4 v = load_pack<ES>(P, mine, i);
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < n && p != w.r) st_plain(os_slot(P, p, par, w.r) + (i - lo), v);
+        }
+        __syncthreads();
+        if (tid < n && tid != w.r) {
+            fence_acq_rel_sys();
+            st_relaxed_sys(flag_ptr(P, tid, F_OS, w.c, w.r), e);
+        }
+        bool ok = true;
+        if (tid < n && tid != w.r) ok = wait_geq(P, flag_ptr(P, w.r, F_OS, w.c, tid), e);
+        if (!__syncthreads_and(ok)) return;
+        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+            uint4 v[kMaxRanks];
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < n) v[p] = (p == w.r) ? load_pack<ES>(P, mine, i) : ld_cg(os_slot(P, w.r, par, p) + (i - lo));
+            Acc<DT> acc;
+            acc_init<DT>(acc, v[0]);
+#pragma unroll
+            for (int p = 1; p < kMaxRanks; ++p)
+                if (p < n) acc_add<DT, OP>(acc, v[p]);
+            store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+        }
+    }
+    if (tid == 0) st->epoch = e0 + nchunks;
+}
+
+template <int DT, int OP>
+__device__ void oneshot_ll(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    const int n = w.n, tid = w.tid;
+    ChanState* st = chan_state(P, w.r, w.c);
+    const uint64_t e0 = st->epoch;
+    const unsigned long long NP = npacks<ES>(P);
+    const unsigned long long CP = P.osll_chunk / 16;
+    const unsigned long long nchunks = (NP + CP - 1) / CP;
+    char* mine = P.bufs[w.r];
+    bool ok = true;
+    for (unsigned long long k = 0; k < nchunks; ++k) {
+        const uint64_t e = e0 + k + 1;
+        const uint32_t f = (uint32_t)e;
+        const int par = (int)(e & 1);
+        const unsigned long long lo = k * CP, hi = (lo + CP < NP) ? lo + CP : NP;
+        unsigned long long a, b;
+        split_range(lo, hi, P.nch, w.c, a, b);
+        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+            const uint4 v = load_pack<ES>(P, mine, i);
+            for (int p = 0; p < n; ++p) {
+                if (p == w.r) continue;
+                uint4* l = osll_slot(P, p, par, w.r) + 2 * (i - lo);
+                st_ll(l, v.x, v.y, f);
+                st_ll(l + 1, v.z, v.w, f);
+            }
+        }
+        for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
+            Acc<DT> acc;
+            for (int p = 0; p < n && ok; ++p) {
+                uint4 v;
+                if (p == w.r) {
+                    v = load_pack<ES>(P, mine, i);
+                } else {
+                    const uint4* l = osll_slot(P, w.r, par, p) + 2 * (i - lo);
+                    uint4 l0, l1;
+                    ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
+                    v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+                }
+                if (p == 0) acc_init<DT>(acc, v);
+                else acc_add<DT, OP>(acc, v);
+            }
+            if (ok) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+        }
+        if (!__syncthreads_and(ok)) return;   // parity reuse safety
+    }
+    if (tid == 0) st->epoch = e0 + nchunks;
+}
+
+// ====================================================================== FIFOs
+// A connection is a kSteps-slot FIFO in the RECEIVER's scratch.  The sender
+// counts slots sent, the receiver slots consumed; both counters persist in the
+// owners' ChanState across calls, so FIFOs never need resetting.
+//   Simple: payload, fence, tail flag (= sent) in the receiver's scratch.
+//   LL    : payload as LL lines whose flag is (u32)(slot sequence + 1).
+//   Both  : the receiver returns a head credit (= consumed) to the sender.
+
+template <int PROTO> struct Fifo;
+
+template <> struct Fifo<POLAR_PROTO_SIMPLE> {
+    // wire packs per slot for `wp` 16-B packs per element-pack
+    static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 16; }
+    static __device__ __forceinline__ void put(uint4* slot, unsigned long long j, uint4 v, uint32_t) { st_plain(slot + j, v); }
+    static __device__ __forceinline__ bool get(const Params&, const uint4* slot, unsigned long long j, uint32_t, uint4& v) {
+        v = ld_cg(slot + j);
+        return true;
+    }
+};
+template <> struct Fifo<POLAR_PROTO_LL> {
+    static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 32; }
+    static __device__ __forceinline__ void put(uint4* slot, unsigned long long j, uint4 v, uint32_t f) {
+        st_ll(slot + 2 * j, v.x, v.y, f);
+        st_ll(slot + 2 * j + 1, v.z, v.w, f);
+    }
+    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long j, uint32_t f, uint4& v) {
+        uint4 l0, l1;
+        if (!poll_ll(P, slot + 2 * j, f, l0) || !poll_ll(P, slot + 2 * j + 1, f, l1)) return false;
+        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+        return true;
+    }
+};
+
+// ======================================================================= ring
+// nch rings in rank order.  Per channel, loop chunks of n sub-chunks; step s of
+// reduce-scatter sends sub-chunk (r - s) mod n to r+1; after n-1 steps rank r
+// holds the full reduction of sub-chunk r+1; n-1 all-gather steps forward it.
+
+template <int PROTO>
+__device__ __forceinline__ uint4* ring_slot(const Params& P, int owner, int c, unsigned long long seq) {
+    const bool ll = PROTO == POLAR_PROTO_LL;
+    const unsigned long long slot = ll ? P.ringll_slot : P.ring_slot;
+    const unsigned long long off = ll ? P.ringll_off : P.ring_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + off + ((size_t)c * kSteps + (seq % kSteps)) * slot);
+}
+
+template <int DT, int OP, int PROTO>
+__device__ void ring(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int AW = AccWords<DT>::N;
+    using F = Fifo<PROTO>;
+    const int n = w.n, tid = w.tid, r = w.r, c = w.c;
+    const int next = (r + 1) % n, prev = (r + n - 1) % n;
+    ChanState* st = chan_state(P, r, c);
+    unsigned long long sent = st->ring_sent, recvd = st->ring_recv;
+    const unsigned long long slot_bytes = PROTO == POLAR_PROTO_LL ? P.ringll_slot : P.ring_slot;
+    const unsigned long long SP = F::slot_packs(slot_bytes) / AW;   // element-packs per slot
+    const unsigned long long NP = npacks<ES>(P);
+    unsigned long long ca, cb;
+    split_range(0, NP, P.nch, c, ca, cb);
+    char* mine = P.bufs[r];
+    uint64_t* head_in = flag_ptr(P, r, F_RING_HEAD, c, 0);     // credits from next
+    uint64_t* tail_in = flag_ptr(P, r, F_RING_TAIL, c, 0);     // fills from prev (Simple)
+    uint64_t* tail_out = flag_ptr(P, next, F_RING_TAIL, c, 0);
+    uint64_t* head_out = flag_ptr(P, prev, F_RING_HEAD, c, 0);
+    const unsigned long long LC = SP * (unsigned long long)n;
+    for (unsigned long long base = ca; base < cb; base += LC) {
+        const unsigned long long L = (cb - base < LC) ? cb - base : LC;
+        for (int s = 0; s < 2 * (n - 1) + 1; ++s) {
+            const bool do_recv = s > 0;
+            const bool do_send = s < 2 * (n - 1);
+            // sub-chunk handled at this step
+            int k;
+            if (s < n) k = ((r - s) % n + n) % n;           // RS steps (s = n-1 finalizes k = r+1)
+            else k = ((r - (s - n) ) % n + n) % n;          // AG step t = s-n receives chunk r - t
+            if (s == n - 1) k = (r + 1) % n;
+            const unsigned long long ks = base + L * (unsigned long long)k / n;
+            const unsigned long long ke = base + L * (unsigned long long)(k + 1) / n;
+            // ---- waits (one thread), then barrier
+            bool ok = true;
+            if (tid == 0) {
+                if (do_recv && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, tail_in, recvd + 1);
+                if (ok && do_send && sent >= (unsigned long long)kSteps) ok = wait_geq(P, head_in, sent - kSteps + 1);
+            }
+            if (!__syncthreads_and(ok)) return;
+            const uint4* src = ring_slot<PROTO>(P, r, c, recvd);
+            uint4* dst = ring_slot<PROTO>(P, next, c, sent);
+            const uint32_t fin = (uint32_t)(recvd + 1), fout = (uint32_t)(sent + 1);
+            for (unsigned long long i = ks + tid; i < ke && ok; i += blockDim.x) {
+                const unsigned long long j = i - ks;
+                if (s == 0) {
+                    Acc<DT> acc;
+                    acc_init<DT>(acc, load_pack<ES>(P, mine, i));
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+                } else if (s < n) {
+                    Acc<DT> acc;
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) ok = ok && F::get(P, src, j * AW + q, fin, acc.w[q]);
+                    if (!ok) break;
+                    acc_add<DT, OP>(acc, load_pack<ES>(P, mine, i));
+                    if (s < n - 1) {
+#pragma unroll
+                        for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+                    } else {
+                        const uint4 out = acc_fin<DT>(acc);
+                        store_pack<ES>(P, mine, i, out);
+                        F::put(dst, j, out, fout);
+                    }
+                } else {
+                    uint4 v;
+                    ok = F::get(P, src, j, fin, v);
+                    if (!ok) break;
+                    store_pack<ES>(P, mine, i, v);
+                    if (do_send) F::put(dst, j, v, fout);
+                }
+            }
+            if (!__syncthreads_and(ok)) return;
+            if (tid == 0) {
+                if (do_send && PROTO == POLAR_PROTO_SIMPLE) {
+                    fence_acq_rel_sys();
+                    st_relaxed_sys(tail_out, sent + 1);
+                }
+                if (do_recv) st_relaxed_sys(head_out, recvd + 1);
+            }
+            if (do_send) ++sent;
+            if (do_recv) ++recvd;
+        }
+    }
+    if (tid == 0) {
+        st->ring_sent = sent;
+        st->ring_recv = recvd;
+    }
+}
+
+// ======================================================================= tree
+// Binary tree per channel over positions pos = (rank - c) mod n (root = rank c
+// mod n); children 2pos+1, 2pos+2.  Up phase: node = own (op) child0 (op)
+// child1, partials (f32 for bf16) sent to the parent slot by slot; the root
+// rounds once and stores.  Down phase: the result flows back down.
+
+template <int PROTO>
+__device__ __forceinline__ uint4* tree_up_slot(const Params& P, int owner, int c, int child, unsigned long long seq) {
+    const bool ll = PROTO == POLAR_PROTO_LL;
+    const unsigned long long slot = ll ? P.treell_slot : P.tree_slot;
+    const unsigned long long off = ll ? P.treell_off : P.tree_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + off + (((size_t)c * 2 + child) * kSteps + (seq % kSteps)) * slot);
+}
+template <int PROTO>
+__device__ __forceinline__ uint4* tree_dn_slot(const Params& P, int owner, int c, unsigned long long seq) {
+    const bool ll = PROTO == POLAR_PROTO_LL;
+    const unsigned long long slot = ll ? P.treell_slot : P.tree_slot;
+    const unsigned long long off = ll ? P.treell_off : P.tree_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + off +
+                                    ((size_t)kMaxCh * 2 * kSteps + (size_t)c * kSteps + (seq % kSteps)) * slot);
+}
+
+template <int DT, int OP, int PROTO>
+__device__ void tree(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int AW = AccWords<DT>::N;
+    using F = Fifo<PROTO>;
+    const int n = w.n, tid = w.tid, r = w.r, c = w.c;
+    const int pos = ((r - c) % n + n) % n;
+    auto rank_of = [&](int q) { return (q + c) % n; };
+    const bool root = pos == 0;
+    const int parent = root ? -1 : rank_of((pos - 1) / 2);
+    const int my_child_idx = root ? 0 : (pos - 1) % 2;
+    int child[2] = {-1, -1};
+    int nchild = 0;
+    for (int k = 0; k < 2; ++k)
+        if (2 * pos + 1 + k < n) { child[k] = rank_of(2 * pos + 1 + k); nchild = k + 1; }
+
+    ChanState* st = chan_state(P, r, c);
+    unsigned long long usent = st->tree_usent, dsent = st->tree_dsent, drecv = st->tree_drecv;
+    unsigned long long urecv[2] = {st->tree_urecv[0], st->tree_urecv[1]};
+    const unsigned long long slot_bytes = PROTO == POLAR_PROTO_LL ? P.treell_slot : P.tree_slot;
+    const unsigned long long SP = F::slot_packs(slot_bytes) / AW;
+    const unsigned long long NP = npacks<ES>(P);
+    unsigned long long ca, cb;
+    split_range(0, NP, P.nch, c, ca, cb);
+    const unsigned long long nslots = (cb - ca + SP - 1) / SP;
+    char* mine = P.bufs[r];
+
+    // ---------------------------------------------------------------- up
+    for (unsigned long long s = 0; s < nslots; ++s) {
+        const unsigned long long lo = ca + s * SP, hi = (lo + SP < cb) ? lo + SP : cb;
+        bool ok = true;
+        if (tid == 0) {
+            if (PROTO == POLAR_PROTO_SIMPLE)
+                for (int k = 0; k < nchild && ok; ++k)
+                    ok = wait_geq(P, flag_ptr(P, r, F_TREE_UTAIL, c, k), urecv[k] + 1);
+            if (ok && !root && usent >= (unsigned long long)kSteps)
+                ok = wait_geq(P, flag_ptr(P, r, F_TREE_UHEAD, c, 0), usent - kSteps + 1);
+        }
+        if (!__syncthreads_and(ok)) return;
+        uint4* dst = root ? nullptr : tree_up_slot<PROTO>(P, parent, c, my_child_idx, usent);
+        const uint32_t fout = (uint32_t)(usent + 1);
+        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+            const unsigned long long j = i - lo;
+            Acc<DT> acc;
+            acc_init<DT>(acc, load_pack<ES>(P, mine, i));
+            for (int k = 0; k < nchild && ok; ++k) {
+                const uint4* src = tree_up_slot<PROTO>(P, r, c, k, urecv[k]);
+                Acc<DT> b;
+#pragma unroll
+                for (int q = 0; q < AW; ++q) ok = ok && F::get(P, src, j * AW + q, (uint32_t)(urecv[k] + 1), b.w[q]);
+                if (ok) acc_merge<DT, OP>(acc, b);
+            }
+            if (!ok) break;
+            if (root) {
+                store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+            } else {
+#pragma unroll
+                for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+            }
+        }
+        if (!__syncthreads_and(ok)) return;
+        if (tid == 0) {
+            if (!root && PROTO == POLAR_PROTO_SIMPLE) {
+                fence_acq_rel_sys();
+                st_relaxed_sys(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1);
+            }
+            for (int k = 0; k < nchild; ++k) st_relaxed_sys(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1);
+        }
+        if (!root) ++usent;
+        for (int k = 0; k < nchild; ++k) ++urecv[k];
+    }
+    // -------------------------------------------------------------- down
+    for (unsigned long long s = 0; s < nslots; ++s) {
+        const unsigned long long lo = ca + s * SP, hi = (lo + SP < cb) ? lo + SP : cb;
+        bool ok = true;
+        if (tid == 0) {
+            if (!root && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), drecv + 1);
+            if (dsent >= (unsigned long long)kSteps)
+                for (int k = 0; k < nchild && ok; ++k)
+                    ok = wait_geq(P, flag_ptr(P, r, F_TREE_DHEAD, c, k), dsent - kSteps + 1);
+        }
+        if (!__syncthreads_and(ok)) return;
+        const uint4* src = root ? nullptr : tree_dn_slot<PROTO>(P, r, c, drecv);
+        const uint32_t fin = (uint32_t)(drecv + 1), fout = (uint32_t)(dsent + 1);
+        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+            const unsigned long long j = i - lo;
+            uint4 v;
+            if (root) {
+                v = load_pack<ES>(P, mine, i);
+            } else {
+                ok = F::get(P, src, j, fin, v);
+                if (!ok) break;
+                store_pack<ES>(P, mine, i, v);
+            }
+            for (int k = 0; k < nchild; ++k) F::put(tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
+        }
+        if (!__syncthreads_and(ok)) return;
+        if (tid == 0) {
+            if (PROTO == POLAR_PROTO_SIMPLE && nchild) {
+                fence_acq_rel_sys();
+                for (int k = 0; k < nchild; ++k) st_relaxed_sys(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1);
+            }
+            if (!root) st_relaxed_sys(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1);
+        }
+        if (nchild) ++dsent;
+        if (!root) ++drecv;
+    }
+    if (tid == 0) {
+        st->tree_usent = usent;
+        st->tree_urecv[0] = urecv[0];
+        st->tree_urecv[1] = urecv[1];
+        st->tree_dsent = dsent;
+        st->tree_drecv = drecv;
+    }
+}
+
+// ================================================================== kernels
+
+template <int DT, int OP, int ALGO, int PROTO>
+__global__ void __launch_bounds__(kBlock, 2) allreduce_kernel(Params P) {
+    const Who w = who(P);
+    if constexpr (ALGO == POLAR_ALGO_TWOSHOT) {
+        if constexpr (PROTO == POLAR_PROTO_SIMPLE) twoshot_simple<DT, OP>(P, w);
+        else twoshot_ll<DT, OP>(P, w);
+    } else if constexpr (ALGO == POLAR_ALGO_ONESHOT) {
+        if constexpr (PROTO == POLAR_PROTO_SIMPLE) oneshot_simple<DT, OP>(P, w);
+        else oneshot_ll<DT, OP>(P, w);
+    } else if constexpr (ALGO == POLAR_ALGO_RING) {
+        ring<DT, OP, PROTO>(P, w);
+    } else {
+        tree<DT, OP, PROTO>(P, w);
+    }
+}
+
+}  // namespace dev
+}  // namespace polar

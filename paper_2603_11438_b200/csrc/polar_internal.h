@@ -1,0 +1,67 @@
+// Internal declarations shared by the host C++ files of libpolar (not installed).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "polar.h"
+
+namespace polar {
+
+polar_status validate_rows(const polar_policy_row* rows, uint32_t nrows);
+polar_status decide_rows(const polar_policy_row* rows, uint32_t nrows, uint32_t generation,
+                         const polar_ctx* ctx, polar_decision* out);
+
+// ----------------------------------------------------------- scratch layout
+// Every rank's scratch has the same layout (offsets identical on all ranks), so a
+// peer's region is peer_scratch[p] + offset.
+constexpr int kMaxRanks = POLAR_MAXRANKS;
+constexpr int kMaxCh = POLAR_MAXCH;
+
+// flag kinds: one 128 B row (8 peers x u64, padded) per (kind, channel)
+enum FlagKind : int {
+    F_ENTRY = 0,     // two-shot: "my buffer is ready"           (written by peer p into slot p)
+    F_EXIT = 1,      // two-shot: "done with your buffer"
+    F_OS = 2,        // one-shot Simple: "my data is in your staging slot"
+    F_RING_TAIL = 3, // ring: sender -> receiver, slots filled     (slot 0)
+    F_RING_HEAD = 4, // ring: receiver -> sender, slots consumed   (slot 0)
+    F_TREE_UTAIL = 5,  // tree up: child k -> parent, slot k (k = 0, 1)
+    F_TREE_UHEAD = 6,  // tree up: parent -> child, slot 0
+    F_TREE_DTAIL = 7,  // tree down: parent -> child, slot 0
+    F_TREE_DHEAD = 8,  // tree down: child k -> parent, slot k
+    F_INIT = 9,        // init barrier
+    F_NKINDS = 10
+};
+constexpr size_t kFlagRow = 128;  // bytes per (kind, channel) row
+constexpr size_t kFlagBytes = (size_t)F_NKINDS * kMaxCh * kFlagRow;
+
+// per-channel persistent counters (local to the rank that owns the scratch)
+struct ChanState {
+    uint64_t epoch;        // one-shot / two-shot handshake epoch
+    uint64_t ring_sent;    // slots sent to next (ring, Simple and LL share the count)
+    uint64_t ring_recv;    // slots consumed from prev
+    uint64_t tree_usent;   // up-slots sent to parent
+    uint64_t tree_urecv[2];// up-slots consumed from child k
+    uint64_t tree_dsent;   // down-slots sent to (each) child
+    uint64_t tree_drecv;   // down-slots consumed from parent
+    uint64_t pad[8];
+};
+constexpr size_t kStateBytes = sizeof(ChanState) * kMaxCh;
+
+struct Layout {
+    size_t flags_off, state_off;
+    size_t os_off, os_chunk;          // one-shot Simple staging: [2][kMaxRanks][os_chunk]
+    size_t osll_off, osll_chunk;      // one-shot LL: [2][kMaxRanks][2*osll_chunk] (payload bytes per slot)
+    size_t tsll_off, tsll_chunk;      // two-shot LL: RS [2][R][2*c] then AG [2][R][2*c]
+    size_t ring_off, ring_slot;       // ring Simple FIFO: [kMaxCh][kSteps][ring_slot]
+    size_t ringll_off, ringll_slot;   // ring LL FIFO: [kMaxCh][kSteps][2*ringll_slot]
+    size_t tree_off, tree_slot;       // tree Simple: up [kMaxCh][2][kSteps][slot], down [kMaxCh][kSteps][slot]
+    size_t treell_off, treell_slot;   // tree LL: same with 2x
+    size_t bounce_off, bounce_bytes;  // two-shot bounce for unregistered buffers (real comms)
+    size_t total;
+};
+constexpr int kSteps = 4;  // FIFO depth (slots) per connection
+
+Layout make_layout(bool with_bounce);
+
+}  // namespace polar

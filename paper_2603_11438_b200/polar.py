@@ -1,0 +1,324 @@
+"""Thin ctypes binding of libpolar (include/polar.h) — argument marshalling only.
+
+Every step of the hot path (decision, dispatch, the kernels) runs inside
+libpolar.so; this module only converts Python/torch arguments to the C ABI.
+If the library is missing it raises at import: there is no Python or CPU
+fallback for any operation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("POLAR_LIB", os.path.join(_HERE, "libpolar.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libpolar.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(there is no fallback implementation)")
+lib = C.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------- enums
+OK, EINVAL, ECUDA, EUNSUPPORTED, ETIMEOUT, EBUSY, ESTATE, ENOMEM = range(8)
+STATUS_NAMES = {OK: "ok", EINVAL: "einval", ECUDA: "ecuda", EUNSUPPORTED: "eunsupported",
+                ETIMEOUT: "etimeout", EBUSY: "ebusy", ESTATE: "estate", ENOMEM: "enomem"}
+INT32, INT64, FLOAT32, BFLOAT16 = 2, 4, 7, 9
+SUM, MAX, MIN = 0, 2, 3
+COLL_ALLREDUCE, COLL_ALLGATHER, COLL_BROADCAST, COLL_REDUCESCATTER = 0, 1, 2, 3
+TREE, RING, NVLS, ONESHOT, TWOSHOT = 0, 1, 2, 3, 4
+LL, LL128, SIMPLE = 0, 1, 2
+UNSET = 0xFFFFFFFF
+MAXCH, MAXRANKS, MAXROWS = 32, 8, 64
+
+DTYPE_CODES = {"i32": INT32, "i64": INT64, "f32": FLOAT32, "bf16": BFLOAT16}
+OP_CODES = {"sum": SUM, "max": MAX, "min": MIN}
+ALGO_CODES = {"tree": TREE, "ring": RING, "nvls": NVLS, "oneshot": ONESHOT, "twoshot": TWOSHOT}
+PROTO_CODES = {"ll": LL, "ll128": LL128, "simple": SIMPLE}
+ALGO_NAMES = {v: k for k, v in ALGO_CODES.items()}
+PROTO_NAMES = {v: k for k, v in PROTO_CODES.items()}
+
+
+class PolarError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{what}: {lib.polar_status_string(status).decode()}")
+
+
+# --------------------------------------------------------------- structs
+class Ctx(C.Structure):
+    _fields_ = [("coll", C.c_uint32), ("nranks", C.c_uint32), ("bytes", C.c_uint64)]
+
+
+class Decision(C.Structure):
+    _fields_ = [("algo", C.c_uint32), ("proto", C.c_uint32), ("nchannels", C.c_uint32),
+                ("generation", C.c_uint32)]
+
+    def as_tuple(self):
+        return (self.algo, self.proto, self.nchannels)
+
+    def __repr__(self):
+        return (f"Decision({ALGO_NAMES.get(self.algo, self.algo)}, {PROTO_NAMES.get(self.proto, self.proto)}, "
+                f"nch={self.nchannels}, gen={self.generation})")
+
+
+class PolicyRow(C.Structure):
+    _fields_ = [("coll", C.c_uint32), ("nranks", C.c_uint32), ("max_bytes", C.c_uint64),
+                ("algo", C.c_uint32), ("proto", C.c_uint32), ("nchannels", C.c_uint32), ("_pad", C.c_uint32)]
+
+
+class BenchStats(C.Structure):
+    _fields_ = [("calls", C.c_uint64), ("p50_ns", C.c_double), ("p99_ns", C.c_double),
+                ("mean_ns", C.c_double), ("min_ns", C.c_double), ("max_ns", C.c_double),
+                ("timer_overhead_ns", C.c_double), ("batched_mean_ns", C.c_double)]
+
+
+class SwapStats(C.Structure):
+    _fields_ = [("calls", C.c_uint64), ("issued", C.c_uint64), ("invalid", C.c_uint64),
+                ("nonmonotonic", C.c_uint64), ("swaps", C.c_uint64), ("rejected", C.c_uint64),
+                ("rejected_changed", C.c_uint64), ("swap_p50_ns", C.c_double), ("swap_p99_ns", C.c_double),
+                ("swap_max_ns", C.c_double), ("final_generation", C.c_uint32)]
+
+
+AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+_P = C.c_void_p
+_sigs = {
+    "polar_set_policy": (C.c_int, [C.POINTER(PolicyRow), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "polar_decide": (C.c_int, [C.POINTER(Ctx), C.POINTER(Decision)]),
+    "polar_decide_batch": (C.c_int, [C.POINTER(Ctx), C.POINTER(Decision), C.c_size_t]),
+    "polar_policy_generation": (C.c_uint32, []),
+    "polar_get_policy": (C.c_int, [C.POINTER(PolicyRow), C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "polar_bench_decide": (C.c_int, [C.POINTER(Ctx), C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
+                                     C.POINTER(BenchStats)]),
+    "polar_bench_swap": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint32, C.POINTER(PolicyRow), C.c_uint32,
+                                   C.POINTER(PolicyRow), C.c_uint32, C.POINTER(SwapStats)]),
+    "polar_comm_init": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int, C.c_int, AG_FN, _P]),
+    "polar_comm_init_virtual": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
+    "polar_comm_destroy": (C.c_int, [_P]),
+    "polar_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "polar_mem_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "polar_mem_free": (C.c_int, [_P, _P]),
+    "polar_register": (C.c_int, [_P, _P, C.c_size_t]),
+    "polar_allreduce": (C.c_int, [_P, _P, C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_allreduce_v": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_allreduce_forced": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, C.POINTER(Decision), _P]),
+    "polar_allreduce_host": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_comm_last_decision": (C.c_int, [_P, C.POINTER(Decision)]),
+    "polar_comm_launches": (C.c_uint64, [_P]),
+    "polar_comm_check": (C.c_int, [_P]),
+    "polar_status_string": (C.c_char_p, [C.c_int]),
+    "polar_version": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _sigs.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sigs)
+
+
+def _check(st, what):
+    if st != OK:
+        raise PolarError(st, what)
+
+
+# ---------------------------------------------------------------- policy
+def rows_array(rows):
+    arr = (PolicyRow * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        arr[i] = PolicyRow(*[int(x) for x in r[:6]], 0)
+    return arr
+
+
+def set_policy_status(rows):
+    """Raw status of polar_set_policy (no raise) and the generation."""
+    arr = rows_array(rows)
+    gen = C.c_uint32(0)
+    st = lib.polar_set_policy(arr, len(rows), C.byref(gen))
+    return st, gen.value
+
+
+def set_policy(rows) -> int:
+    st, gen = set_policy_status(rows)
+    _check(st, "polar_set_policy")
+    return gen
+
+
+def decide(nranks: int, nbytes: int, coll: int = COLL_ALLREDUCE) -> Decision:
+    d = Decision()
+    _check(lib.polar_decide(C.byref(Ctx(coll, nranks, nbytes)), C.byref(d)), "polar_decide")
+    return d
+
+
+def decide_batch(ctxs):
+    """ctxs: list of (nranks, nbytes) -> list of (algo, proto, nch, generation)."""
+    n = len(ctxs)
+    a = (Ctx * max(1, n))()
+    for i, (nr, b) in enumerate(ctxs):
+        a[i] = Ctx(COLL_ALLREDUCE, nr, b)
+    out = (Decision * max(1, n))()
+    _check(lib.polar_decide_batch(a, out, n), "polar_decide_batch")
+    return [(d.algo, d.proto, d.nchannels, d.generation) for d in out[:n]]
+
+
+def generation() -> int:
+    return lib.polar_policy_generation()
+
+
+def get_policy():
+    arr = (PolicyRow * MAXROWS)()
+    n, g = C.c_uint32(0), C.c_uint32(0)
+    _check(lib.polar_get_policy(arr, MAXROWS, C.byref(n), C.byref(g)), "polar_get_policy")
+    return [(r.coll, r.nranks, r.max_bytes, r.algo, r.proto, r.nchannels) for r in arr[:n.value]], g.value
+
+
+def bench_decide(ctxs, nwarm=10_000, ncalls=400_000):
+    a = (Ctx * len(ctxs))()
+    for i, (nr, b) in enumerate(ctxs):
+        a[i] = Ctx(COLL_ALLREDUCE, nr, b)
+    s = BenchStats()
+    _check(lib.polar_bench_decide(a, len(ctxs), nwarm, ncalls, None, C.byref(s)), "polar_bench_decide")
+    return {k: getattr(s, k) for k, _ in BenchStats._fields_}
+
+
+def bench_swap(rows_a, rows_b, nthreads=4, calls_per_thread=100_000, nswaps=1000):
+    s = SwapStats()
+    _check(lib.polar_bench_swap(nthreads, calls_per_thread, nswaps, rows_array(rows_a), len(rows_a),
+                                rows_array(rows_b), len(rows_b), C.byref(s)), "polar_bench_swap")
+    return {k: getattr(s, k) for k, _ in SwapStats._fields_}
+
+
+# ---------------------------------------------------------------- comms
+def _torch_dtype_code(t):
+    import torch
+    m = {torch.int32: INT32, torch.int64: INT64, torch.float32: FLOAT32, torch.bfloat16: BFLOAT16}
+    if t.dtype not in m:
+        raise PolarError(EINVAL, f"dtype {t.dtype} not supported")
+    return m[t.dtype]
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ wrapper so torch can view library memory."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+class Comm:
+    """A communicator: ``Comm.virtual(n)`` (n ranks on one GPU) or
+    ``Comm.init(n, rank, device, allgather)`` (one rank per process)."""
+
+    def __init__(self, handle, keep=None):
+        self.h = C.c_void_p(handle)
+        self._keep = keep
+        nr, rk, nl = C.c_int(), C.c_int(), C.c_int()
+        _check(lib.polar_comm_info(self.h, C.byref(nr), C.byref(rk), C.byref(nl)), "polar_comm_info")
+        self.nranks, self.rank, self.nlocal = nr.value, rk.value, nl.value
+
+    @classmethod
+    def virtual(cls, nranks: int, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.polar_comm_init_virtual(C.byref(h), nranks, device), "polar_comm_init_virtual")
+        return cls(h.value)
+
+    @classmethod
+    def init(cls, nranks: int, rank: int, device: int, allgather):
+        """allgather(bytes) -> list[bytes] of every rank's payload (rank order)."""
+
+        def _cb(send, recv, nbytes, _user):
+            try:
+                mine = C.string_at(send, nbytes)
+                allb = allgather(mine)
+                C.memmove(recv, b"".join(allb), nbytes * len(allb))
+                return 0
+            except Exception:  # noqa: BLE001 - must not unwind through C
+                return 1
+
+        cb = AG_FN(_cb)
+        h = C.c_void_p()
+        _check(lib.polar_comm_init(C.byref(h), nranks, rank, device, cb, None), "polar_comm_init")
+        return cls(h.value, keep=cb)
+
+    def destroy(self):
+        if self.h:
+            _check(lib.polar_comm_destroy(self.h), "polar_comm_destroy")
+            self.h = C.c_void_p()
+
+    def mem_alloc(self, nbytes: int):
+        """Symmetric device memory: list of nlocal raw pointers."""
+        ptrs = (C.c_void_p * self.nlocal)()
+        _check(lib.polar_mem_alloc(self.h, nbytes, ptrs), "polar_mem_alloc")
+        return [int(p) for p in ptrs]
+
+    def mem_alloc_tensors(self, numel: int, dtype):
+        """Symmetric allocation viewed as torch tensors (one per local rank)."""
+        import torch
+        es = torch.empty(0, dtype=dtype).element_size()
+        out = []
+        for p in self.mem_alloc(numel * es):
+            t = torch.as_tensor(_CudaArray(p, numel * es), device="cuda").view(dtype)
+            out.append(t)
+        return out
+
+    def mem_free(self, ptr: int):
+        _check(lib.polar_mem_free(self.h, C.c_void_p(ptr)), "polar_mem_free")
+
+    def register(self, tensor):
+        _check(lib.polar_register(self.h, C.c_void_p(tensor.data_ptr()), tensor.numel() * tensor.element_size()),
+               "polar_register")
+
+    def _bufs(self, tensors):
+        if not isinstance(tensors, (list, tuple)):
+            tensors = [tensors]
+        if len(tensors) != self.nlocal:
+            raise PolarError(EINVAL, f"need {self.nlocal} buffers, got {len(tensors)}")
+        arr = (C.c_void_p * self.nlocal)(*[t.data_ptr() for t in tensors])
+        t0 = tensors[0]
+        return arr, t0.numel(), _torch_dtype_code(t0)
+
+    def allreduce(self, tensors, op="sum", stream=None):
+        """In-place policy-selected AllReduce (one kernel launch)."""
+        arr, n, dt = self._bufs(tensors)
+        _check(lib.polar_allreduce_v(self.h, arr, n, dt, OP_CODES[op], _stream_ptr(stream)), "polar_allreduce_v")
+
+    def allreduce_raw(self, ptrs, count, dtype_code, op_code, stream_ptr):
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        return lib.polar_allreduce_v(self.h, arr, count, dtype_code, op_code, C.c_void_p(stream_ptr))
+
+    def allreduce_forced(self, tensors, algo, proto, nch, op="sum", stream=None):
+        arr, n, dt = self._bufs(tensors)
+        d = Decision(ALGO_CODES[algo] if isinstance(algo, str) else algo,
+                     PROTO_CODES[proto] if isinstance(proto, str) else proto, nch, 0)
+        _check(lib.polar_allreduce_forced(self.h, arr, n, dt, OP_CODES[op], C.byref(d), _stream_ptr(stream)),
+               "polar_allreduce_forced")
+
+    def allreduce_host(self, host_tensors, dev_tensors, op="sum", stream=None):
+        harr, n, dt = self._bufs(host_tensors)
+        darr, _, _ = self._bufs(dev_tensors)
+        _check(lib.polar_allreduce_host(self.h, harr, darr, n, dt, OP_CODES[op], _stream_ptr(stream)),
+               "polar_allreduce_host")
+
+    def last_decision(self) -> Decision:
+        d = Decision()
+        _check(lib.polar_comm_last_decision(self.h, C.byref(d)), "polar_comm_last_decision")
+        return d
+
+    def launches(self) -> int:
+        return lib.polar_comm_launches(self.h)
+
+    def check(self):
+        _check(lib.polar_comm_check(self.h), "polar_comm_check")
+
+
+def version() -> str:
+    return lib.polar_version().decode()
