@@ -35,6 +35,51 @@ template <int ES> __device__ __forceinline__ unsigned long long npacks(const Par
     return (P.count + (16 / ES) - 1) / (16 / ES);
 }
 
+// One-shot / two-shot epochs are PER CALL, not per channel: every channel's
+// ChanState.epoch holds the same value and each call advances all kMaxCh of
+// them (CTA c writes channels c, c+nch, ...).  Staging is shared by all
+// channels, so a per-channel epoch could let channel c' see channel c's stale LL
+// line carrying the same flag value after the channel count changed.
+__device__ __forceinline__ void epoch_publish(const Params& P, const Who& w, uint64_t e) {
+    if (w.tid == 0)
+        for (int cc = w.c; cc < kMaxCh; cc += P.nch) chan_state(P, w.r, cc)->epoch = e;
+}
+
+// Staged (one-shot / two-shot LL) chunk geometry.  Each chunk gives every
+// channel a FIXED region of `per` packs inside a staging slot (offset c*per), so
+// no two channels ever share a staging location, whatever the chunk (a short
+// last chunk must not re-slice: a lagging peer channel may still be polling the
+// same-parity slot of two chunks ago).  `per` is the same on every rank and for
+// every chunk of a call: min(slot capacity / nch, ceil(NP / (parts*nch))),
+// rounded to whole 512-B units.
+struct Geo {
+    unsigned long long per;      // packs per channel per part per chunk
+    unsigned long long part;     // per * nch: packs per part (owner) per chunk
+    unsigned long long chunk;    // part * parts
+    unsigned long long nchunks;
+};
+__device__ __forceinline__ Geo make_geo(unsigned long long NP, unsigned long long cap_packs, int nch, int parts) {
+    Geo g;
+    unsigned long long cap = (cap_packs / (unsigned long long)nch) / kUnit * kUnit;
+    unsigned long long need = (NP + (unsigned long long)(parts * nch) - 1) / (unsigned long long)(parts * nch);
+    need = (need + kUnit - 1) / kUnit * kUnit;
+    g.per = need < cap ? need : cap;
+    if (g.per < kUnit) g.per = kUnit;
+    g.part = g.per * (unsigned long long)nch;
+    g.chunk = g.part * (unsigned long long)parts;
+    g.nchunks = (NP + g.chunk - 1) / g.chunk;
+    return g;
+}
+// channel c's packs of part j in chunk k: [lo, hi) and the slot offset of lo
+__device__ __forceinline__ void geo_slice(const Geo& g, unsigned long long NP, unsigned long long k, int j, int c,
+                                          unsigned long long& lo, unsigned long long& hi, unsigned long long& off) {
+    off = g.per * (unsigned long long)c;
+    lo = k * g.chunk + g.part * (unsigned long long)j + off;
+    hi = lo + g.per;
+    if (lo > NP) lo = NP;
+    if (hi > NP) hi = NP;
+}
+
 // ===================================================================== two-shot
 // Simple, zero-copy on symmetric buffers: entry barrier; owner r reads shard r
 // from every rank, reduces in rank order, stores the result into every rank's
@@ -78,7 +123,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     ok = true;
     if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
     if (!__syncthreads_and(ok)) return;
-    if (tid == 0) st->epoch = e;
+    epoch_publish(P, w, e);
 }
 
 // Two-shot LL: push-based.  RS: rank r writes its part of owner j's shard as LL
@@ -102,76 +147,60 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const unsigned long long SC = P.tsll_chunk / 16;   // packs per owner per chunk
-    const unsigned long long CH = SC * (unsigned long long)n;
-    const unsigned long long nchunks = (NP + CH - 1) / CH;
+    const Geo g = make_geo(NP, P.tsll_chunk / 16, P.nch, n);
     char* mine = P.bufs[w.r];
     bool ok = true;
-    for (unsigned long long k = 0; k < nchunks; ++k) {
+    for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
         const uint32_t f = (uint32_t)e;
         const int par = (int)(e & 1);
-        const unsigned long long clo = k * CH;
+        unsigned long long lo, hi, off;
         // RS push: my contribution to every other owner's part
-        for (int j = 0; j < n && ok; ++j) {
+        for (int j = 0; j < n; ++j) {
             if (j == w.r) continue;
-            unsigned long long plo = clo + SC * j, phi = plo + SC;
-            if (plo > NP) plo = NP;
-            if (phi > NP) phi = NP;
-            unsigned long long a, b;
-            split_range(plo, phi, P.nch, w.c, a, b);
-            uint4* dst = tsll_rs(P, j, par, w.r);
-            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
-                uint4 v = load_pack<ES>(P, mine, i);
-                uint4* l = dst + 2 * (i - plo);
+            geo_slice(g, NP, k, j, w.c, lo, hi, off);
+            uint4* dst = tsll_rs(P, j, par, w.r) + 2 * off;
+            for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
+                const uint4 v = load_pack<ES>(P, mine, i);
+                uint4* l = dst + 2 * (i - lo);
                 st_ll(l, v.x, v.y, f);
                 st_ll(l + 1, v.z, v.w, f);
             }
         }
-        // reduce my part, push result to every rank
-        {
-            unsigned long long plo = clo + SC * w.r, phi = plo + SC;
-            if (plo > NP) plo = NP;
-            if (phi > NP) phi = NP;
-            unsigned long long a, b;
-            split_range(plo, phi, P.nch, w.c, a, b);
-            for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
-                Acc<DT> acc;
-                for (int p = 0; p < n && ok; ++p) {
-                    uint4 v;
-                    if (p == w.r) {
-                        v = load_pack<ES>(P, mine, i);
-                    } else {
-                        const uint4* l = tsll_rs(P, w.r, par, p) + 2 * (i - plo);
-                        uint4 l0, l1;
-                        ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
-                        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
-                    }
-                    if (p == 0) acc_init<DT>(acc, v);
-                    else acc_add<DT, OP>(acc, v);
+        // reduce my part in rank order, keep it and push it to every rank
+        geo_slice(g, NP, k, w.r, w.c, lo, hi, off);
+        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+            Acc<DT> acc;
+            for (int p = 0; p < n && ok; ++p) {
+                uint4 v;
+                if (p == w.r) {
+                    v = load_pack<ES>(P, mine, i);
+                } else {
+                    const uint4* l = tsll_rs(P, w.r, par, p) + 2 * (off + i - lo);
+                    uint4 l0, l1;
+                    ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
+                    v = make_uint4(l0.x, l0.z, l1.x, l1.z);
                 }
-                if (!ok) break;
-                const uint4 out = acc_fin<DT>(acc);
-                store_pack<ES>(P, mine, i, out);
-                for (int p = 0; p < n; ++p) {
-                    if (p == w.r) continue;
-                    uint4* l = tsll_ag(P, p, par, w.r) + 2 * (i - plo);
-                    st_ll(l, out.x, out.y, f);
-                    st_ll(l + 1, out.z, out.w, f);
-                }
+                if (p == 0) acc_init<DT>(acc, v);
+                else acc_add<DT, OP>(acc, v);
+            }
+            if (!ok) break;
+            const uint4 out = acc_fin<DT>(acc);
+            store_pack<ES>(P, mine, i, out);
+            for (int p = 0; p < n; ++p) {
+                if (p == w.r) continue;
+                uint4* l = tsll_ag(P, p, par, w.r) + 2 * (off + i - lo);
+                st_ll(l, out.x, out.y, f);
+                st_ll(l + 1, out.z, out.w, f);
             }
         }
         // AG receive: results of every other owner
         for (int j = 0; j < n && ok; ++j) {
             if (j == w.r) continue;
-            unsigned long long plo = clo + SC * j, phi = plo + SC;
-            if (plo > NP) plo = NP;
-            if (phi > NP) phi = NP;
-            unsigned long long a, b;
-            split_range(plo, phi, P.nch, w.c, a, b);
-            const uint4* src = tsll_ag(P, w.r, par, j);
-            for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
-                const uint4* l = src + 2 * (i - plo);
+            geo_slice(g, NP, k, j, w.c, lo, hi, off);
+            const uint4* src = tsll_ag(P, w.r, par, j) + 2 * off;
+            for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+                const uint4* l = src + 2 * (i - lo);
                 uint4 l0, l1;
                 ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
                 if (ok) store_pack<ES>(P, mine, i, make_uint4(l0.x, l0.z, l1.x, l1.z));
@@ -179,7 +208,7 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
         }
         if (!__syncthreads_and(ok)) return;   // parity reuse safety
     }
-    if (tid == 0) st->epoch = e0 + nchunks;
+    epoch_publish(P, w, e0 + g.nchunks);
 }
 
 // ===================================================================== one-shot
@@ -202,20 +231,18 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const unsigned long long CP = P.os_chunk / 16;
-    const unsigned long long nchunks = (NP + CP - 1) / CP;
+    const Geo g = make_geo(NP, P.os_chunk / 16, P.nch, 1);
     char* mine = P.bufs[w.r];
-    for (unsigned long long k = 0; k < nchunks; ++k) {
+    for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
         const int par = (int)(e & 1);
-        const unsigned long long lo = k * CP, hi = (lo + CP < NP) ? lo + CP : NP;
-        unsigned long long a, b;
-        split_range(lo, hi, P.nch, w.c, a, b);
-        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+        unsigned long long lo, hi, off;
+        geo_slice(g, NP, k, 0, w.c, lo, hi, off);
+        for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
             const uint4 v = load_pack<ES>(P, mine, i);
 #pragma unroll
             for (int p = 0; p < kMaxRanks; ++p)
-                if (p < n && p != w.r) st_plain(os_slot(P, p, par, w.r) + (i - lo), v);
+                if (p < n && p != w.r) st_plain(os_slot(P, p, par, w.r) + off + (i - lo), v);
         }
         __syncthreads();
         if (tid < n && tid != w.r) {
@@ -225,11 +252,11 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
         bool ok = true;
         if (tid < n && tid != w.r) ok = wait_geq(P, flag_ptr(P, w.r, F_OS, w.c, tid), e);
         if (!__syncthreads_and(ok)) return;
-        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+        for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
             uint4 v[kMaxRanks];
 #pragma unroll
             for (int p = 0; p < kMaxRanks; ++p)
-                if (p < n) v[p] = (p == w.r) ? load_pack<ES>(P, mine, i) : ld_cg(os_slot(P, w.r, par, p) + (i - lo));
+                if (p < n) v[p] = (p == w.r) ? load_pack<ES>(P, mine, i) : ld_cg(os_slot(P, w.r, par, p) + off + (i - lo));
             Acc<DT> acc;
             acc_init<DT>(acc, v[0]);
 #pragma unroll
@@ -238,7 +265,7 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
             store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
         }
     }
-    if (tid == 0) st->epoch = e0 + nchunks;
+    epoch_publish(P, w, e0 + g.nchunks);
 }
 
 template <int DT, int OP>
@@ -248,34 +275,32 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const unsigned long long CP = P.osll_chunk / 16;
-    const unsigned long long nchunks = (NP + CP - 1) / CP;
+    const Geo g = make_geo(NP, P.osll_chunk / 16, P.nch, 1);
     char* mine = P.bufs[w.r];
     bool ok = true;
-    for (unsigned long long k = 0; k < nchunks; ++k) {
+    for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
         const uint32_t f = (uint32_t)e;
         const int par = (int)(e & 1);
-        const unsigned long long lo = k * CP, hi = (lo + CP < NP) ? lo + CP : NP;
-        unsigned long long a, b;
-        split_range(lo, hi, P.nch, w.c, a, b);
-        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+        unsigned long long lo, hi, off;
+        geo_slice(g, NP, k, 0, w.c, lo, hi, off);
+        for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
             const uint4 v = load_pack<ES>(P, mine, i);
             for (int p = 0; p < n; ++p) {
                 if (p == w.r) continue;
-                uint4* l = osll_slot(P, p, par, w.r) + 2 * (i - lo);
+                uint4* l = osll_slot(P, p, par, w.r) + 2 * (off + i - lo);
                 st_ll(l, v.x, v.y, f);
                 st_ll(l + 1, v.z, v.w, f);
             }
         }
-        for (unsigned long long i = a + tid; i < b && ok; i += blockDim.x) {
+        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
             Acc<DT> acc;
             for (int p = 0; p < n && ok; ++p) {
                 uint4 v;
                 if (p == w.r) {
                     v = load_pack<ES>(P, mine, i);
                 } else {
-                    const uint4* l = osll_slot(P, w.r, par, p) + 2 * (i - lo);
+                    const uint4* l = osll_slot(P, w.r, par, p) + 2 * (off + i - lo);
                     uint4 l0, l1;
                     ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
                     v = make_uint4(l0.x, l0.z, l1.x, l1.z);
@@ -287,7 +312,7 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
         }
         if (!__syncthreads_and(ok)) return;   // parity reuse safety
     }
-    if (tid == 0) st->epoch = e0 + nchunks;
+    epoch_publish(P, w, e0 + g.nchunks);
 }
 
 // ====================================================================== FIFOs

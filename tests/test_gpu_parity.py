@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element
+(virtual ranks on one B200).  Every algorithm x
+protocol x dtype x op, sizes spanning several tiles/chunks and ragged tails,
+edge cases (count 0/1, count < nranks, unaligned buffers, back-to-back calls
+alternating algorithms without a host sync), and the policy-selected path whose
+recorded decision must equal the oracle's decision mapping.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import policy as OP
+from tests.gpu_common import check_result, default_dist, to_device, to_host
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2603_11438_b200 import polar as L  # noqa: E402
+
+ALGOS = ["oneshot", "twoshot", "ring", "tree"]
+PROTOS = ["ll", "simple"]
+_COMMS = {}
+
+
+def comm(n):
+    """Cached virtual comm; a comm with a latched error is unusable by design
+    (polar.h), so it is replaced rather than letting one failure cascade."""
+    c = _COMMS.get(n)
+    if c is not None:
+        try:
+            c.check()
+        except L.PolarError:
+            c = None
+    if c is None:
+        torch.cuda.synchronize()
+        c = _COMMS[n] = L.Comm.virtual(n, 0)
+    return c
+
+
+def run(n, dtype, op, count, algo, proto, nch, dist=None, cfg=1, offset=0):
+    xs = synth.gen_ranks(dtype, count, n, cfg=cfg, dist=dist or default_dist(dtype))
+    ts = [to_device(x, dtype, offset) for x in xs]
+    c = comm(n)
+    c.allreduce_forced(ts, algo, proto, nch, op=op)
+    torch.cuda.synchronize()
+    c.check()
+    got = [to_host(t, dtype) for t in ts]
+    check_result(got, xs, dtype, op, algo, n)
+    d = c.last_decision()
+    assert (L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto]) == (algo, proto)
+
+
+@pytest.mark.parametrize("algo,proto", list(itertools.product(ALGOS, PROTOS)))
+@pytest.mark.parametrize("dtype", synth.DTYPES)
+def test_matrix_sum(algo, proto, dtype):
+    for n in (2, 3, 8):
+        for count, nch in ((1, 1), (7, 2), (1000, 3), (40_003, 4), (300_001, 8)):
+            run(n, dtype, "sum", count, algo, proto, nch)
+
+
+@pytest.mark.parametrize("algo,proto", list(itertools.product(ALGOS, PROTOS)))
+@pytest.mark.parametrize("op", ["max", "min"])
+@pytest.mark.parametrize("dtype", synth.DTYPES)
+def test_matrix_max_min(algo, proto, op, dtype):
+    for n, count, nch in ((4, 12_345, 3), (8, 999, 1)):
+        run(n, dtype, op, count, algo, proto, nch)
+
+
+@pytest.mark.parametrize("algo,proto", list(itertools.product(ALGOS, PROTOS)))
+def test_exact_integer_valued_floats(algo, proto):
+    """Integer-valued inputs: every algorithm must match bit for bit."""
+    for dtype in ("f32", "bf16"):
+        xs = synth.gen_ranks(dtype, 77_777, 8, cfg=4, dist="ints")
+        ts = [to_device(x, dtype) for x in xs]
+        c = comm(8)
+        c.allreduce_forced(ts, algo, proto, 5)
+        torch.cuda.synchronize()
+        from oracle import allreduce as orc
+        exp = orc.allreduce(xs, dtype, "sum")
+        for t in ts:
+            assert np.array_equal(to_host(t, dtype), exp)
+
+
+@pytest.mark.parametrize("algo,proto", list(itertools.product(ALGOS, PROTOS)))
+def test_edges(algo, proto):
+    for n in (2, 8):
+        run(n, "f32", "sum", 0, algo, proto, 1)           # no-op
+        run(n, "f32", "sum", 1, algo, proto, 32)          # count < nranks, more channels than packs
+        run(n, "i32", "sum", n - 1, algo, proto, 2)
+        run(n, "bf16", "sum", 9, algo, proto, 3)          # one full pack + 1
+        run(n, "i64", "sum", 4097, algo, proto, 7, offset=1)    # unaligned buffers
+        run(n, "bf16", "sum", 5000, algo, proto, 2, offset=3)
+
+
+@pytest.mark.parametrize("algo,proto", list(itertools.product(ALGOS, PROTOS)))
+def test_multi_chunk(algo, proto):
+    """Sizes beyond one staging chunk / FIFO loop chunk, max channels."""
+    run(8, "f32", "sum", (3 << 20) + 17, algo, proto, 32)
+    run(2, "bf16", "sum", (5 << 20) + 3, algo, proto, 16)
+
+
+def test_back_to_back_alternating_no_sync():
+    """Consecutive calls of different algorithms/protocols/channel counts on one
+    stream, without host synchronisation (epochs, FIFO counters, parities)."""
+    n, dtype = 8, "f32"
+    c = comm(n)
+    rng = np.random.default_rng(11)
+    combos = list(itertools.product(ALGOS, PROTOS))
+    xs_list, ts_list = [], []
+    for it in range(24):
+        algo, proto = combos[rng.integers(len(combos))]
+        count = int(rng.integers(1, 200_000))
+        xs = synth.gen_ranks(dtype, count, n, cfg=100 + it, dist="ints")
+        ts = [to_device(x, dtype) for x in xs]
+        c.allreduce_forced(ts, algo, proto, int(rng.integers(1, 33)))
+        xs_list.append((xs, algo))
+        ts_list.append(ts)
+    torch.cuda.synchronize()
+    c.check()
+    for (xs, algo), ts in zip(xs_list, ts_list):
+        check_result([to_host(t, dtype) for t in ts], xs, dtype, "sum", algo, n)
+
+
+def test_policy_selected_decision_matches_oracle():
+    """polar_allreduce (policy-selected): recorded decision == oracle mapping."""
+    rows = [(0, 0, 16 << 10, OP.ONESHOT, OP.LL, 2), (0, 0, 256 << 10, OP.TWOSHOT, OP.LL, 4),
+            (0, 8, 2 << 20, OP.RING, OP.SIMPLE, 6), (0, 0, 4 << 20, OP.TREE, OP.UNSET, 0)]
+    L.set_policy(rows)
+    try:
+        for n in (2, 8):
+            c = comm(n)
+            for count in (2, 4096, 65_536, 300_000, 1 << 20, 3 << 20):
+                xs = synth.gen_ranks("f32", count, n, cfg=7, dist="ints")
+                ts = [to_device(x, "f32") for x in xs]
+                c.allreduce(ts)
+                torch.cuda.synchronize()
+                d = c.last_decision()
+                exp = OP.decide(rows, 0, n, count * 4)
+                assert d.as_tuple() == exp
+                from oracle import allreduce as orc
+                ref = orc.allreduce(xs, "f32", "sum")
+                for t in ts:
+                    assert np.array_equal(to_host(t, "f32"), ref)
+    finally:
+        L.set_policy([])
+
+
+def test_default_policy_bench_size_sampled():
+    """Full bench size (C2: 8 ranks x 128 MiB f32, the launch config bench.py
+    times): sampled windows checked against the oracle one by one."""
+    from oracle import allreduce as orc
+    n, count = 8, 32 << 20
+    xs = synth.gen_ranks("f32", count, n, cfg=2, dist="unif")
+    c = comm(n)
+    ts = [to_device(x, "f32") for x in xs]
+    c.allreduce(ts)
+    torch.cuda.synchronize()
+    c.check()
+    rng = np.random.default_rng(5)
+    windows = [(0, 4096), (count - 4099, count)] + [(int(s), int(s) + 2048) for s in rng.integers(0, count - 2048, 16)]
+    for lo, hi in windows:
+        exp = orc.allreduce([x[lo:hi] for x in xs], "f32", "sum")
+        for t in ts:
+            got = to_host(t[lo:hi], "f32")
+            assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), (lo, hi)
