@@ -61,7 +61,15 @@ def _compile(src, verbose):
     return obj
 
 
-def build(verbose: bool = True, force: bool = False) -> str:
+def build(verbose: bool = True, force: bool = False, defines=(), lib=None, build_dir=None) -> str:
+    """defines: extra -D flags (tuning variants); lib/build_dir: alternate outputs."""
+    global BUILD, LIB, CU_FLAGS, COMMON
+    if defines or lib or build_dir:
+        BUILD = build_dir or BUILD
+        LIB = lib or LIB
+        extra = [f"-D{d}" for d in defines]
+        CU_FLAGS = CU_FLAGS + extra
+        COMMON = COMMON + extra
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
     hdrs = _headers()
@@ -81,4 +89,12 @@ def build(verbose: bool = True, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    # python -m paper_2603_11438_b200.build [--force] [--variant NAME -DX=1 ...]
+    argv = sys.argv[1:]
+    if "--variant" in argv:
+        name = argv[argv.index("--variant") + 1]
+        defs = [a[2:] for a in argv if a.startswith("-D")]
+        build(force=True, defines=defs, lib=os.path.join(ROOT, "build", f"variants/libpolar_{name}.so"),
+              build_dir=os.path.join(ROOT, "build", f"obj_{name}"))
+    else:
+        build(force="--force" in argv)

@@ -14,7 +14,16 @@ namespace dev {
 
 // ------------------------------------------------------------- kernel params
 
-constexpr int kBlock = 512;   // threads per CTA (one CTA per rank-channel)
+#ifndef POLAR_BLOCK
+#define POLAR_BLOCK 512
+#endif
+#ifndef POLAR_LB_MIN
+#define POLAR_LB_MIN 2      // min resident CTAs per SM requested from ptxas (register cap)
+#endif
+#ifndef POLAR_TS_UNROLL
+#define POLAR_TS_UNROLL 1   // packs per thread per two-shot iteration
+#endif
+constexpr int kBlock = POLAR_BLOCK;   // threads per CTA (one CTA per rank-channel)
 
 struct Params {
     char* bufs[kMaxRanks];     // rank p's data for this call (peer-mapped; zero-copy two-shot uses all)

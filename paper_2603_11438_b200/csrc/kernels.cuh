@@ -100,20 +100,36 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     unsigned long long s0, s1, a, b;
     split_range(0, NP, n, w.r, s0, s1);
     split_range(s0, s1, P.nch, w.c, a, b);
-    for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
-        uint4 v[kMaxRanks];
+    // 2 packs per thread per iteration: 2n independent 16-B loads in flight
+    // before the first store (memory-level parallelism for HBM / NVLink latency)
+    constexpr int U = POLAR_TS_UNROLL;
+    const unsigned long long stride = (unsigned long long)blockDim.x;
+    for (unsigned long long i0 = a + tid; i0 < b; i0 += U * stride) {
+        uint4 v[U][kMaxRanks];
 #pragma unroll
-        for (int p = 0; p < kMaxRanks; ++p)
-            if (p < n) v[p] = load_pack<ES>(P, P.bufs[p], i);
-        Acc<DT> acc;
-        acc_init<DT>(acc, v[0]);
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + u * stride;
+            if (i < b) {
 #pragma unroll
-        for (int p = 1; p < kMaxRanks; ++p)
-            if (p < n) acc_add<DT, OP>(acc, v[p]);
-        const uint4 out = acc_fin<DT>(acc);
+                for (int p = 0; p < kMaxRanks; ++p)
+                    if (p < n) v[u][p] = load_pack<ES>(P, P.bufs[p], i);
+            }
+        }
 #pragma unroll
-        for (int p = 0; p < kMaxRanks; ++p)
-            if (p < n) store_pack<ES>(P, P.bufs[p], i, out);
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + u * stride;
+            if (i < b) {
+                Acc<DT> acc;
+                acc_init<DT>(acc, v[u][0]);
+#pragma unroll
+                for (int p = 1; p < kMaxRanks; ++p)
+                    if (p < n) acc_add<DT, OP>(acc, v[u][p]);
+                const uint4 out = acc_fin<DT>(acc);
+#pragma unroll
+                for (int p = 0; p < kMaxRanks; ++p)
+                    if (p < n) store_pack<ES>(P, P.bufs[p], i, out);
+            }
+        }
     }
     __syncthreads();
     if (tid < n) {
@@ -591,7 +607,7 @@ __device__ void tree(const Params& P, const Who& w) {
 // ================================================================== kernels
 
 template <int DT, int OP, int ALGO, int PROTO>
-__global__ void __launch_bounds__(kBlock, 2) allreduce_kernel(Params P) {
+__global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params P) {
     const Who w = who(P);
     if constexpr (ALGO == POLAR_ALGO_TWOSHOT) {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) twoshot_simple<DT, OP>(P, w);

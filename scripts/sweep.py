@@ -56,6 +56,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warm", type=int, default=5)
     ap.add_argument("--max-time", type=float, default=0.05, help="skip configs slower than this (s/call)")
+    ap.add_argument("--graph", action="store_true", help="time K calls captured in one CUDA graph (device time, no host launch cost)")
     args = ap.parse_args()
     n, dt = args.n, args.dtype
     comm = L.Comm.virtual(n, 0)
@@ -76,7 +77,14 @@ def main():
                                       "skipped": f"{t1*1e6:.0f} us"}), flush=True)
                     continue
                 iters = max(3, min(args.iters, int(0.2 / max(t1, 1e-6))))
-                t = time_calls(fn, args.warm, iters)
+                if args.graph:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        for _ in range(iters):
+                            fn()
+                    t = time_calls(g.replay, 2, 3) / iters
+                else:
+                    t = time_calls(fn, args.warm, iters)
                 comm.check()
                 bus = size * 2 * (n - 1) / n / t / 1e9
                 hbm = 2 * n * size / t / 1e9

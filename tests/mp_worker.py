@@ -1,0 +1,107 @@
+"""One rank of a real (multi-process) polar comm, launched by torchrun.
+
+Each rank: gloo process group for the host bootstrap only, polar_comm_init
+(CUDA IPC exchange of the scratch), then every algorithm x protocol on this
+rank's seeded input, checked against the oracle (each rank regenerates every
+rank's input itself).  Also the registered zero-copy two-shot (polar_mem_alloc)
+and the unregistered two-shot bounce path.  Rank 0 writes a JSON report.
+
+Device: LOCAL_RANK if that many GPUs exist, else GPU 0 for every rank (ranks
+then share one GPU through CUDA IPC and context time-slicing).
+"""
+import hashlib
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from oracle import allreduce as orc  # noqa: E402
+from paper_2603_11438_b200 import polar as L  # noqa: E402
+from tests.gpu_common import to_device, to_host  # noqa: E402
+
+
+def main():
+    out_path = sys.argv[1]
+    rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = local if torch.cuda.device_count() > local else 0
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
+
+    def allgather(b):
+        o = [None] * ws
+        dist.all_gather_object(o, b)
+        return o
+
+    comm = L.Comm.init(ws, rank, dev, allgather)
+    results = []
+
+    def check(tag, t, xs, dtype, op, exact):
+        got = to_host(t, dtype)
+        exp = orc.allreduce(xs, dtype, op)
+        if exact:
+            ok = np.array_equal(got.view(np.uint8), exp.view(np.uint8))
+        else:
+            bound = 1e-6 * ws * np.sum(np.abs(np.stack(xs).astype(np.float64)), axis=0)
+            ok = bool(np.all(np.abs(got.astype(np.float64) - exp.astype(np.float64)) <= bound))
+        # cross-rank bitwise identity: gather a hash of the result
+        h = hashlib.sha1(got.tobytes()).hexdigest()
+        hs = [None] * ws
+        dist.all_gather_object(hs, h)
+        results.append({"tag": tag, "rank": rank, "ok": bool(ok), "identical": len(set(hs)) == 1})
+
+    for algo in ("oneshot", "twoshot", "ring", "tree"):
+        for proto in ("ll", "simple"):
+            for dtype, count, nch in (("f32", 70_001, 3), ("bf16", 5_003, 2), ("i32", 1, 1)):
+                xs = synth.gen_ranks(dtype, count, ws, cfg=31, dist="ints")
+                t = to_device(xs[rank], dtype)
+                comm.allreduce_forced(t, algo, proto, nch)
+                torch.cuda.synchronize()
+                comm.check()
+                check(f"{algo}/{proto}/{dtype}/{count}", t, xs, dtype, "sum", True)
+    # registered zero-copy two-shot on symmetric memory, random floats: exact (rank order)
+    count = 1 << 20
+    xs = synth.gen_ranks("f32", count, ws, cfg=32, dist="unif")
+    (buf,) = comm.mem_alloc_tensors(count, torch.float32)
+    buf.copy_(torch.from_numpy(xs[rank]))
+    comm.allreduce_forced(buf, "twoshot", "simple", 8)
+    torch.cuda.synchronize()
+    check("twoshot/simple/registered", buf, xs, "f32", "sum", True)
+    # policy-selected on a plain torch tensor (unregistered: bounce path if two-shot)
+    t = to_device(xs[rank], "f32")
+    comm.allreduce(t)
+    torch.cuda.synchronize()
+    d = comm.last_decision()
+    check(f"policy/{L.ALGO_NAMES[d.algo]}/{L.PROTO_NAMES[d.proto]}", t, xs, "f32", "sum",
+          L.ALGO_NAMES[d.algo] in ("oneshot", "twoshot"))
+    # back-to-back without host sync, alternating algorithms
+    ts, xss = [], []
+    for i, (algo, proto) in enumerate([("ring", "ll"), ("twoshot", "simple"), ("tree", "simple"),
+                                       ("oneshot", "ll"), ("twoshot", "ll"), ("ring", "simple")]):
+        xs = synth.gen_ranks("i32", 30_000 + i, ws, cfg=40 + i, dist="full")
+        t = to_device(xs[rank], "i32")
+        comm.allreduce_forced(t, algo, proto, 1 + i)
+        ts.append(t)
+        xss.append((xs, algo))
+    torch.cuda.synchronize()
+    comm.check()
+    for (xs, algo), t in zip(xss, ts):
+        check(f"b2b/{algo}", t, xs, "i32", "sum", True)
+    comm.destroy()
+    allres = [None] * ws
+    dist.all_gather_object(allres, results)
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump([r for rr in allres for r in rr], f)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,45 @@
+"""Real multi-process comms (polar_comm_init + CUDA IPC), one process per rank,
+launched with torchrun on 127.0.0.1.  On a 1-GPU box every rank shares GPU 0
+(IPC between processes on one device; kernels time-slice), which exercises the
+whole real-comm path — bootstrap all-gather, IPC mapping, per-process launches,
+flags across contexts — except NVLink itself."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_multiprocess_ipc_all_algorithms(tmp_path, nranks):
+    out = tmp_path / "mp.json"
+    env = dict(os.environ)
+    env.setdefault("POLAR_TIMEOUT_MS", "60000")
+    env["POLAR_BOUNCE"] = str(1 << 20)   # small bounce buffer: exercise the chunked bounce path
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "tests", "mp_worker.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    res = json.loads(out.read_text())
+    bad = [x for x in res if not (x["ok"] and x["identical"])]
+    assert not bad, bad
+    assert len(res) == nranks * (4 * 2 * 3 + 2 + 6)
