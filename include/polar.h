@@ -177,6 +177,14 @@ polar_status polar_bench_swap(uint32_t nthreads, uint64_t calls_per_thread, uint
 polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_device,
                              polar_allgather_fn ag, void* user);
 
+/* Host bootstrap self-check (collective; no GPU needed): all-gathers a 32-B
+ * record {magic, nranks, rank, scratch-layout hash} through `ag` and verifies
+ * that every rank agrees on nranks and on the scratch layout (the POLAR_* size
+ * variables) and that slot p holds rank p.  POLAR_OK, POLAR_EINVAL (bad args),
+ * or POLAR_ESTATE (disagreement or callback failure).  polar_comm_init runs the
+ * same check before it exchanges any IPC handle. */
+polar_status polar_bootstrap_check(int nranks, int rank, polar_allgather_fn ag, void* user);
+
 /* Virtual comm: nranks logical ranks hosted by THIS process on ONE device; one
  * kernel launch runs every rank's CTAs (grid = nranks x nchannels, a cooperative
  * launch so that cross-rank waits cannot deadlock).  Same kernels, same

@@ -244,6 +244,36 @@ polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks])
     return POLAR_OK;
 }
 
+struct BootRec {
+    uint64_t magic;
+    uint32_t nranks, rank;
+    uint64_t layout_hash;
+    uint64_t pad;
+};
+static_assert(sizeof(BootRec) == 32, "bootstrap record is 32 B");
+constexpr uint64_t kBootMagic = 0x706f6c6172763031ull;   // "polarv01"
+
+uint64_t layout_hash(const Layout& L) {
+    // FNV-1a over the layout (every offset/size must match across ranks)
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&L);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(Layout); ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgather_fn ag, void* user) {
+    BootRec mine{kBootMagic, (uint32_t)nranks, (uint32_t)rank, layout_hash(L), 0};
+    std::vector<BootRec> all(nranks);
+    if (ag(&mine, all.data(), sizeof(BootRec), user) != 0) return POLAR_ESTATE;
+    for (int p = 0; p < nranks; ++p) {
+        const BootRec& r = all[p];
+        if (r.magic != kBootMagic || r.nranks != (uint32_t)nranks || r.rank != (uint32_t)p ||
+            r.layout_hash != mine.layout_hash)
+            return POLAR_ESTATE;
+    }
+    return POLAR_OK;
+}
+
 polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int dtype, int op,
                           const polar_decision* forced, cudaStream_t stream) {
     const int es = esize_of(dtype);
@@ -350,11 +380,17 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     if (st == POLAR_OK) st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[0]), c->L.total));
     if (st == POLAR_OK) st = cuerr(cudaMemset(c->scratch_own[0], 0, c->L.total));
     if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
+    if (st == POLAR_OK) st = bootstrap_check(nranks, rank, c->L, ag, user);
     if (st == POLAR_OK) st = exchange_and_map(c, c->scratch_own[0], c->scratch);
     if (st == POLAR_OK) st = init_barrier(c);
     if (st != POLAR_OK) { destroy_comm(c); return st; }
     *out = c;
     return POLAR_OK;
+}
+
+polar_status polar_bootstrap_check(int nranks, int rank, polar_allgather_fn ag, void* user) {
+    if (nranks < 1 || nranks > POLAR_MAXRANKS || rank < 0 || rank >= nranks || !ag) return POLAR_EINVAL;
+    return bootstrap_check(nranks, rank, make_layout(true), ag, user);
 }
 
 polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device) {

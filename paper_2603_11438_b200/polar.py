@@ -95,6 +95,7 @@ _sigs = {
                                    C.POINTER(PolicyRow), C.c_uint32, C.POINTER(SwapStats)]),
     "polar_comm_init": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int, C.c_int, AG_FN, _P]),
     "polar_comm_init_virtual": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
+    "polar_bootstrap_check": (C.c_int, [C.c_int, C.c_int, AG_FN, _P]),
     "polar_comm_destroy": (C.c_int, [_P]),
     "polar_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "polar_mem_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
@@ -214,6 +215,26 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
 
+def _make_ag(allgather):
+    """Wrap allgather(bytes) -> list[bytes] as the C callback polar_allgather_fn."""
+
+    def _cb(send, recv, nbytes, _user):
+        try:
+            allb = allgather(C.string_at(send, nbytes))
+            C.memmove(recv, b"".join(allb), nbytes * len(allb))
+            return 0
+        except Exception:  # noqa: BLE001 - must not unwind through C
+            return 1
+
+    return AG_FN(_cb)
+
+
+def bootstrap_check(nranks: int, rank: int, allgather) -> int:
+    """Raw status of polar_bootstrap_check (collective, host only)."""
+    cb = _make_ag(allgather)
+    return lib.polar_bootstrap_check(nranks, rank, cb, None)
+
+
 class Comm:
     """A communicator: ``Comm.virtual(n)`` (n ranks on one GPU) or
     ``Comm.init(n, rank, device, allgather)`` (one rank per process)."""
@@ -235,16 +256,7 @@ class Comm:
     def init(cls, nranks: int, rank: int, device: int, allgather):
         """allgather(bytes) -> list[bytes] of every rank's payload (rank order)."""
 
-        def _cb(send, recv, nbytes, _user):
-            try:
-                mine = C.string_at(send, nbytes)
-                allb = allgather(mine)
-                C.memmove(recv, b"".join(allb), nbytes * len(allb))
-                return 0
-            except Exception:  # noqa: BLE001 - must not unwind through C
-                return 1
-
-        cb = AG_FN(_cb)
+        cb = _make_ag(allgather)
         h = C.c_void_p()
         _check(lib.polar_comm_init(C.byref(h), nranks, rank, device, cb, None), "polar_comm_init")
         return cls(h.value, keep=cb)
