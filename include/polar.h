@@ -238,6 +238,13 @@ polar_status polar_allreduce_forced(polar_comm_t comm, void* const* bufs, size_t
 polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, void* const* dev_bufs,
                                   size_t count, polar_dtype dtype, polar_op op, void* stream);
 
+/* Host enqueue cost (BASELINE config 4 "host enqueue ns per call"): ncalls
+ * back-to-back polar_allreduce_v calls (decide + dispatch + launch, no sync)
+ * timed with a monotonic clock; *ns_per_call = wall time / ncalls.  The stream
+ * is synchronised before and after the timed loop. */
+polar_status polar_bench_enqueue(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype,
+                                 polar_op op, void* stream, uint64_t ncalls, double* ns_per_call);
+
 /* Decision used by the most recent AllReduce on this comm. */
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);
 
@@ -247,6 +254,12 @@ uint64_t polar_comm_launches(polar_comm_t comm);
 /* Latched asynchronous errors (device timeouts); POLAR_OK if none.  Does not
  * synchronise: a timeout becomes visible once the kernel that hit it ended. */
 polar_status polar_comm_check(polar_comm_t comm);
+
+/* Diagnostics: when dev_buf is non-NULL, every CTA of every later AllReduce on
+ * this comm writes 4 %globaltimer stamps (ns) to dev_buf[4*cta + k] (kernel
+ * dependent points; two-shot: start, after entry barrier, loop end, exit).
+ * bytes must hold nlocal*32*4 u64.  NULL disables. */
+polar_status polar_comm_set_trace(polar_comm_t comm, void* dev_buf, size_t bytes);
 
 const char* polar_status_string(polar_status s);
 

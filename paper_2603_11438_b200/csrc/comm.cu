@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -28,7 +29,7 @@ namespace dev {
 __global__ void init_barrier_kernel(Params P, unsigned long long value) {
     const int r = P.rank0 + (int)blockIdx.x;
     const int tid = (int)threadIdx.x;
-    if (tid < P.nranks) st_release_sys(flag_ptr(P, tid, F_INIT, 0, r), value);
+    if (tid < P.nranks) st_release(flag_ptr(P, tid, F_INIT, 0, r), value, P.sys);
     bool ok = true;
     if (tid < P.nranks) ok = wait_geq(P, flag_ptr(P, r, F_INIT, 0, tid), value);
     __syncthreads_and(ok);
@@ -101,6 +102,9 @@ struct polar_comm_s {
     void* user = nullptr;
     uint64_t init_value = 0;
     int max_coop_blocks = 0;             // virtual: co-residency bound
+    unsigned long long* trace = nullptr; // diagnostic per-CTA timestamps
+    bool coop = true;                    // virtual: cooperative launch (co-residency guaranteed)
+    bool pdl = true;                     // programmatic dependent launch (POLAR_PDL=0 disables)
     unsigned long long timeout_ns = 0;
     std::mutex mu;
 };
@@ -142,6 +146,8 @@ void fill_params(const polar_comm_s* c, dev::Params& P) {
     P.ringll_off = L.ringll_off; P.ringll_slot = L.ringll_slot;
     P.tree_off = L.tree_off; P.tree_slot = L.tree_slot;
     P.treell_off = L.treell_off; P.treell_slot = L.treell_slot;
+    P.trace = c->trace;
+    P.sys = c->is_virtual ? 0 : 1;
 }
 
 polar_status check_latched(polar_comm_s* c) {
@@ -153,11 +159,32 @@ polar_status check_latched(polar_comm_s* c) {
 
 polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int grid, cudaStream_t stream) {
     void* args[] = {&P};
-    cudaError_t e;
-    if (c->is_virtual) {
-        e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(dev::kBlock), args, 0, stream);
-    } else {
-        e = cudaLaunchKernel(fn, dim3(grid), dim3(dev::kBlock), args, 0, stream);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(dev::kBlock);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[2];
+    unsigned n = 0;
+    if (c->is_virtual && c->coop) {
+        attrs[n].id = cudaLaunchAttributeCooperative;
+        attrs[n].val.cooperative = 1;
+        ++n;
+    }
+    if (c->pdl) {
+        attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = n;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess && c->pdl) {
+        // PDL not accepted together with the other attributes here: disable it for this comm
+        (void)cudaGetLastError();
+        c->pdl = false;
+        cfg.numAttrs = n - 1;
+        e = cudaLaunchKernelExC(&cfg, fn, args);
     }
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
@@ -184,6 +211,10 @@ polar_status init_barrier(polar_comm_s* c) {
 }
 
 polar_status alloc_common(polar_comm_s* c) {
+    {
+        const char* ev = std::getenv("POLAR_PDL");
+        c->pdl = !(ev && ev[0] == '0');
+    }
     c->timeout_ns = (unsigned long long)env_size("POLAR_TIMEOUT_MS", 20000) * 1000000ull;
     CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
     *c->err_host = 0;
@@ -403,6 +434,11 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
     c->nlocal = nranks;
     c->device = cuda_device;
     c->is_virtual = true;
+    {
+        // POLAR_VIRTUAL_COOP=0: plain launch (diagnostic; co-residency then relies on an idle GPU)
+        const char* ev = std::getenv("POLAR_VIRTUAL_COOP");
+        c->coop = !(ev && ev[0] == '0');
+    }
     c->L = make_layout(false);
     polar_status st = cuerr(cudaSetDevice(cuda_device));
     if (st == POLAR_OK) st = alloc_common(c);
@@ -557,6 +593,31 @@ uint64_t polar_comm_launches(polar_comm_t comm) { return comm ? comm->launches :
 
 polar_status polar_comm_check(polar_comm_t comm) {
     if (!comm) return POLAR_EINVAL;
+    return check_latched(comm);
+}
+
+polar_status polar_comm_set_trace(polar_comm_t comm, void* dev_buf, size_t bytes) {
+    if (!comm || (dev_buf && bytes < (size_t)comm->nlocal * POLAR_MAXCH * 4 * sizeof(unsigned long long)))
+        return POLAR_EINVAL;
+    comm->trace = reinterpret_cast<unsigned long long*>(dev_buf);
+    return POLAR_OK;
+}
+
+polar_status polar_bench_enqueue(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype,
+                                 polar_op op, void* stream, uint64_t ncalls, double* ns_per_call) {
+    if (!comm || !ns_per_call || ncalls == 0) return POLAR_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    polar_status st = do_allreduce(comm, bufs, count, dtype, op, nullptr, s);   // warm
+    if (st != POLAR_OK) return st;
+    CU_TRY(cudaStreamSynchronize(s));
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t i = 0; i < ncalls; ++i) {
+        st = do_allreduce(comm, bufs, count, dtype, op, nullptr, s);
+        if (st != POLAR_OK) return st;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    CU_TRY(cudaStreamSynchronize(s));
+    *ns_per_call = std::chrono::duration<double, std::nano>(t1 - t0).count() / (double)ncalls;
     return check_latched(comm);
 }
 

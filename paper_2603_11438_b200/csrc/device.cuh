@@ -18,7 +18,7 @@ namespace dev {
 #define POLAR_BLOCK 512
 #endif
 #ifndef POLAR_LB_MIN
-#define POLAR_LB_MIN 2      // min resident CTAs per SM requested from ptxas (register cap)
+#define POLAR_LB_MIN 1      // min resident CTAs per SM requested from ptxas (register cap; 2 spills)
 #endif
 #ifndef POLAR_TS_UNROLL
 #define POLAR_TS_UNROLL 1   // packs per thread per two-shot iteration
@@ -40,7 +40,10 @@ struct Params {
     unsigned long long os_off, os_chunk, osll_off, osll_chunk, tsll_off, tsll_chunk;
     unsigned long long ring_off, ring_slot, ringll_off, ringll_slot;
     unsigned long long tree_off, tree_slot, treell_off, treell_slot;
+    unsigned long long* trace;  // optional per-CTA timestamps (polar_comm_set_trace), else null
+    int sys;                    // 1: peers are other GPUs (system-scope ordering); 0: one GPU (gpu scope)
 };
+
 
 // -------------------------------------------------------------- raw memory ops
 
@@ -50,18 +53,32 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Diagnostic: CTA b records %globaltimer at point k (0..3) into trace[4b+k].
+__device__ __forceinline__ void trace_point(const Params& P, int k) {
+    if (P.trace && threadIdx.x == 0) P.trace[4 * blockIdx.x + k] = globaltimer();
 }
-__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+
+// Flag operations at system scope (peers on other GPUs over NVLink) or gpu scope
+// (virtual ranks: every peer is on this GPU, so gpu-scope ordering suffices and
+// avoids MEMBAR.SYS).  `sys` is uniform per launch.
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, int sys) {
+    if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, int sys) {
+    if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, int sys) {
     uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel(int sys) {
+    if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 
 // data loads that must not hit a stale L1 line (peer data, staging reused within a kernel)
 __device__ __forceinline__ uint4 ld_cg(const uint4* p) {
@@ -99,10 +116,10 @@ __device__ __forceinline__ void raise_error(const Params& P, int code) {
 
 // Spin until *p >= v; false on timeout (error latched).
 static __device__ __noinline__ bool wait_geq(const Params& P, const uint64_t* p, uint64_t v) {
-    if (ld_acquire_sys(p) >= v) return true;
+    if (ld_acquire(p, P.sys) >= v) return true;
     const uint64_t t0 = globaltimer();
     for (uint32_t it = 1;; ++it) {
-        if (ld_acquire_sys(p) >= v) return true;
+        if (ld_acquire(p, P.sys) >= v) return true;
         if ((it & 255) == 0) {
             if (globaltimer() - t0 > P.timeout_ns) {
                 raise_error(P, POLAR_ETIMEOUT);

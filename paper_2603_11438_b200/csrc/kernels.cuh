@@ -91,54 +91,87 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     const int n = w.n, tid = w.tid;
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e = st->epoch + 1;
-    if (tid < n) st_release_sys(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e);
+    trace_point(P, 0);
+    if (tid < n) st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
     bool ok = true;
     if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
     if (!__syncthreads_and(ok)) return;
+    trace_point(P, 1);
 
+    // Owner r's shard [s0, s1) is processed by its nch CTAs with DYNAMIC chunk
+    // scheduling: CTAs grab chunk indices from a per-owner counter in the
+    // owner's scratch (ChanState[0].work = (epoch << 32) | next), so a slower
+    // SM takes fewer chunks (static slices left a ~15 % loop-time spread,
+    // measured with polar_comm_set_trace).  Big chunks first, then small ones
+    // for the last nch*kBig packs so the tail is balanced too.
     const unsigned long long NP = npacks<ES>(P);
-    unsigned long long s0, s1, a, b;
+    unsigned long long s0, s1;
     split_range(0, NP, n, w.r, s0, s1);
-    split_range(s0, s1, P.nch, w.c, a, b);
-    // 2 packs per thread per iteration: 2n independent 16-B loads in flight
-    // before the first store (memory-level parallelism for HBM / NVLink latency)
-    constexpr int U = POLAR_TS_UNROLL;
-    const unsigned long long stride = (unsigned long long)blockDim.x;
-    for (unsigned long long i0 = a + tid; i0 < b; i0 += U * stride) {
-        uint4 v[U][kMaxRanks];
+    const unsigned long long L = s1 - s0;
+    constexpr unsigned long long kBig = 2048, kSmall = 256;   // packs (32 KiB / 4 KiB per buffer)
+    const unsigned long long tail = L < (unsigned long long)P.nch * kBig ? L : (unsigned long long)P.nch * kBig;
+    const unsigned long long nbig = (L - tail) / kBig;
+    const unsigned long long bigend = nbig * kBig;
+    const unsigned long long nchunks = nbig + (L - bigend + kSmall - 1) / kSmall;
+    const unsigned long long nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
+    unsigned long long* work = reinterpret_cast<unsigned long long*>(&chan_state(P, w.r, 0)->work);
+    const unsigned long long wbase = (unsigned long long)e << 32;
+    __shared__ unsigned long long s_next;
+    if (tid == 0) {
+        atomicMax(work, wbase);
+        s_next = atomicAdd(work, 1ull) - wbase;
+    }
+    __syncthreads();
+    unsigned long long k = s_next;
+    const uint4* src[kMaxRanks];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned long long i = i0 + u * stride;
-            if (i < b) {
+    for (int p = 0; p < kMaxRanks; ++p) src[p] = reinterpret_cast<const uint4*>(P.bufs[p < n ? p : 0]);
+    while (k < nchunks) {
+        __syncthreads();                                   // everyone has read s_next
+        if (tid == 0) s_next = atomicAdd(work, 1ull) - wbase;   // prefetch the next grab
+        const unsigned long long a = s0 + (k < nbig ? k * kBig : bigend + (k - nbig) * kSmall);
+        unsigned long long b = a + (k < nbig ? kBig : kSmall);
+        if (b > s1) b = s1;
+        if (b <= nfull) {
+            // fast path: full aligned packs, hoisted bases, 2n... loads in flight
+            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+                uint4 v[kMaxRanks];
 #pragma unroll
                 for (int p = 0; p < kMaxRanks; ++p)
-                    if (p < n) v[u][p] = load_pack<ES>(P, P.bufs[p], i);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned long long i = i0 + u * stride;
-            if (i < b) {
+                    if (p < n) v[p] = ld_cg(src[p] + i);
                 Acc<DT> acc;
-                acc_init<DT>(acc, v[u][0]);
+                acc_init<DT>(acc, v[0]);
 #pragma unroll
                 for (int p = 1; p < kMaxRanks; ++p)
-                    if (p < n) acc_add<DT, OP>(acc, v[u][p]);
+                    if (p < n) acc_add<DT, OP>(acc, v[p]);
                 const uint4 out = acc_fin<DT>(acc);
 #pragma unroll
                 for (int p = 0; p < kMaxRanks; ++p)
-                    if (p < n) store_pack<ES>(P, P.bufs[p], i, out);
+                    if (p < n) const_cast<uint4*>(src[p])[i] = out;
+            }
+        } else {
+            // partial last pack / unaligned buffers: element-exact copies
+            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+                Acc<DT> acc;
+                acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0], i));
+                for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p], i));
+                const uint4 out = acc_fin<DT>(acc);
+                for (int p = 0; p < n; ++p) store_pack<ES>(P, P.bufs[p], i, out);
             }
         }
+        __syncthreads();                                   // chunk done, s_next visible
+        k = s_next;
     }
     __syncthreads();
+    trace_point(P, 2);
     if (tid < n) {
-        fence_acq_rel_sys();
-        st_relaxed_sys(flag_ptr(P, tid, F_EXIT, w.c, w.r), e);
+        fence_acq_rel(P.sys);
+        st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
     }
     ok = true;
     if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
     if (!__syncthreads_and(ok)) return;
+    trace_point(P, 3);
     epoch_publish(P, w, e);
 }
 
@@ -262,8 +295,8 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
         }
         __syncthreads();
         if (tid < n && tid != w.r) {
-            fence_acq_rel_sys();
-            st_relaxed_sys(flag_ptr(P, tid, F_OS, w.c, w.r), e);
+            fence_acq_rel(P.sys);
+            st_relaxed(flag_ptr(P, tid, F_OS, w.c, w.r), e, P.sys);
         }
         bool ok = true;
         if (tid < n && tid != w.r) ok = wait_geq(P, flag_ptr(P, w.r, F_OS, w.c, tid), e);
@@ -451,10 +484,10 @@ __device__ void ring(const Params& P, const Who& w) {
             if (!__syncthreads_and(ok)) return;
             if (tid == 0) {
                 if (do_send && PROTO == POLAR_PROTO_SIMPLE) {
-                    fence_acq_rel_sys();
-                    st_relaxed_sys(tail_out, sent + 1);
+                    fence_acq_rel(P.sys);
+                    st_relaxed(tail_out, sent + 1, P.sys);
                 }
-                if (do_recv) st_relaxed_sys(head_out, recvd + 1);
+                if (do_recv) st_relaxed(head_out, recvd + 1, P.sys);
             }
             if (do_send) ++sent;
             if (do_recv) ++recvd;
@@ -551,10 +584,10 @@ __device__ void tree(const Params& P, const Who& w) {
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (!root && PROTO == POLAR_PROTO_SIMPLE) {
-                fence_acq_rel_sys();
-                st_relaxed_sys(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1);
+                fence_acq_rel(P.sys);
+                st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1, P.sys);
             }
-            for (int k = 0; k < nchild; ++k) st_relaxed_sys(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1);
+            for (int k = 0; k < nchild; ++k) st_relaxed(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1, P.sys);
         }
         if (!root) ++usent;
         for (int k = 0; k < nchild; ++k) ++urecv[k];
@@ -587,10 +620,10 @@ __device__ void tree(const Params& P, const Who& w) {
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (PROTO == POLAR_PROTO_SIMPLE && nchild) {
-                fence_acq_rel_sys();
-                for (int k = 0; k < nchild; ++k) st_relaxed_sys(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1);
+                fence_acq_rel(P.sys);
+                for (int k = 0; k < nchild; ++k) st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1, P.sys);
             }
-            if (!root) st_relaxed_sys(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1);
+            if (!root) st_relaxed(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1, P.sys);
         }
         if (nchild) ++dsent;
         if (!root) ++drecv;
@@ -608,6 +641,12 @@ __device__ void tree(const Params& P, const Who& w) {
 
 template <int DT, int OP, int ALGO, int PROTO>
 __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params P) {
+    // Programmatic dependent launch: let the NEXT polar launch on this stream get
+    // its CTAs scheduled during our tail, and wait here until the previous grid
+    // has completed and its memory is visible (== plain stream order; no-ops
+    // when the launch carries no PDL attribute).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const Who w = who(P);
     if constexpr (ALGO == POLAR_ALGO_TWOSHOT) {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) twoshot_simple<DT, OP>(P, w);

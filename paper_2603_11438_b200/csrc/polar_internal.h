@@ -44,7 +44,8 @@ struct ChanState {
     uint64_t tree_urecv[2];// up-slots consumed from child k
     uint64_t tree_dsent;   // down-slots sent to (each) child
     uint64_t tree_drecv;   // down-slots consumed from parent
-    uint64_t pad[8];
+    uint64_t work;         // two-shot dynamic chunk counter: (epoch << 32) | next chunk (channel 0 only)
+    uint64_t pad[7];
 };
 constexpr size_t kStateBytes = sizeof(ChanState) * kMaxCh;
 

@@ -108,6 +108,9 @@ _sigs = {
     "polar_comm_last_decision": (C.c_int, [_P, C.POINTER(Decision)]),
     "polar_comm_launches": (C.c_uint64, [_P]),
     "polar_comm_check": (C.c_int, [_P]),
+    "polar_comm_set_trace": (C.c_int, [_P, _P, C.c_size_t]),
+    "polar_bench_enqueue": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P, C.c_uint64,
+                                      C.POINTER(C.c_double)]),
     "polar_status_string": (C.c_char_p, [C.c_int]),
     "polar_version": (C.c_char_p, []),
 }
@@ -320,6 +323,14 @@ class Comm:
         _check(lib.polar_allreduce_host(self.h, harr, darr, n, dt, OP_CODES[op], _stream_ptr(stream)),
                "polar_allreduce_host")
 
+    def bench_enqueue(self, tensors, ncalls=2000, op="sum", stream=None) -> float:
+        """Host ns per polar_allreduce_v call (decide + dispatch + launch), native loop."""
+        arr, n, dt = self._bufs(tensors)
+        ns = C.c_double(0)
+        _check(lib.polar_bench_enqueue(self.h, arr, n, dt, OP_CODES[op], _stream_ptr(stream), ncalls, C.byref(ns)),
+               "polar_bench_enqueue")
+        return ns.value
+
     def last_decision(self) -> Decision:
         d = Decision()
         _check(lib.polar_comm_last_decision(self.h, C.byref(d)), "polar_comm_last_decision")
@@ -327,6 +338,14 @@ class Comm:
 
     def launches(self) -> int:
         return lib.polar_comm_launches(self.h)
+
+    def set_trace(self, tensor=None):
+        """Diagnostics: per-CTA %globaltimer stamps into a uint64/int64 device tensor (None = off)."""
+        if tensor is None:
+            _check(lib.polar_comm_set_trace(self.h, None, 0), "polar_comm_set_trace")
+        else:
+            _check(lib.polar_comm_set_trace(self.h, C.c_void_p(tensor.data_ptr()),
+                                            tensor.numel() * tensor.element_size()), "polar_comm_set_trace")
 
     def check(self):
         _check(lib.polar_comm_check(self.h), "polar_comm_check")
