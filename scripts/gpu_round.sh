@@ -25,6 +25,11 @@ for w in $WHAT; do
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:allreduce_kernel -s 5 -c 1 \
         -f -o gpurun_out/prof_$TAG python bench.py --steps 8 --warmup 3 > gpurun_out/ncu_full_$TAG.log 2>&1
       echo "ncu full rc=$?" ;;
+    configs)
+      timeout 2400 python scripts/report_configs.py > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err
+      echo "configs rc=$?"; tail -3 gpurun_out/configs_$TAG.jsonl | cut -c1-300 ;;
+    c4)
+      timeout 900 python scripts/c4_latency.py > gpurun_out/c4_$TAG.jsonl 2>&1; echo "c4 rc=$?" ;;
     sweep)
       timeout 900 python scripts/sweep.py --n 8 --dtype f32 > gpurun_out/sweep_f32_$TAG.jsonl 2>&1
       echo "sweep rc=$?" ;;

@@ -166,3 +166,18 @@ def test_decision_cost_bench_sane():
     assert s["calls"] == 100_000
     assert 0 < s["batched_mean_ns"] < 2000
     assert s["p50_ns"] <= s["p99_ns"]
+
+
+def test_committed_policy_files_validate():
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pdir = os.path.join(root, "policies")
+    for name in sorted(os.listdir(pdir)):
+        rows = [tuple(r) for r in json.load(open(os.path.join(pdir, name)))["rows"]]
+        exp = OP.validate(rows)
+        st, _ = L.set_policy_status(rows)
+        assert L.STATUS_NAMES[st] == exp, name
+        assert exp == ("eunsupported" if name == "nvlink_ring_mid_v2.json" else "ok"), name
+        if exp == "ok":
+            _compare(rows)
