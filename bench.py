@@ -255,6 +255,7 @@ def run_polar(args):
     torch.cuda.synchronize()
     comm.check()
     decision = comm.last_decision()
+    launched_nch = comm.launched_channels()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -307,7 +308,8 @@ def run_polar(args):
         t = max_over_ranks(a.elapsed_time(b) / 1e3 / it)
         d = comm.last_decision()
         sweep[str(sz)] = {"busbw_gbs": round(busbw(sz, n, t), 1), "us": round(t * 1e6, 1),
-                          "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels]}
+                          "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
+                          "launched_channels": comm.launched_channels()}
     comm.check()
 
     # e2e: through the C-ABI with HOST buffers; H2D + allreduce + D2H inside the timed region
@@ -342,7 +344,8 @@ def run_polar(args):
             "vs_baseline": round(value / PAPER_8GPU_128MIB_DEFAULT, 4) if (real and n == 8) else None,
             "dtype": "f32", "data": "synthetic", "config": workload_config(n, real),
             "decision": {"algo": L.ALGO_NAMES[decision.algo], "proto": L.PROTO_NAMES[decision.proto],
-                         "nchannels": decision.nchannels, "generation": decision.generation},
+                         "nchannels": decision.nchannels, "generation": decision.generation,
+                         "launched_channels": launched_nch},
             "algbw_gbs": round(S_BYTES / t_step / 1e9, 2),
             "nvlink_frac": round(value / 900.0, 4) if real else None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -248,6 +248,11 @@ polar_status polar_bench_enqueue(polar_comm_t comm, void* const* bufs, size_t co
 /* Decision used by the most recent AllReduce on this comm. */
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);
 
+/* Channels actually launched by the most recent AllReduce (a virtual comm
+ * clamps the decision to co-resident CTAs / nranks) and its grid size
+ * (nchannels x nlocal).  Either pointer may be NULL. */
+polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint32_t* grid);
+
 /* Number of kernels this comm has launched so far (evidence for bench.py). */
 uint64_t polar_comm_launches(polar_comm_t comm);
 

@@ -51,7 +51,7 @@ KiB, MiB = 1024, 1024 * 1024
 DEFAULT_ROWS = [
     (COLL_ALLREDUCE, 0, 64 * KiB, ONESHOT, LL, 4),
     (COLL_ALLREDUCE, 0, 1 * MiB, ONESHOT, SIMPLE, 8),
-    (COLL_ALLREDUCE, 0, U64_MAX, TWOSHOT, SIMPLE, 16),
+    (COLL_ALLREDUCE, 0, U64_MAX, TWOSHOT, SIMPLE, 32),
 ]
 
 

@@ -96,6 +96,7 @@ struct polar_comm_s {
     int* err_host = nullptr;
     int* err_dev = nullptr;
     polar_decision last{};
+    uint32_t last_nch = 0;
     uint64_t launches = 0;
     polar_status latched = POLAR_OK;
     polar_allgather_fn ag = nullptr;
@@ -328,11 +329,12 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     }
     const void* fn = kernel_for(dtype, op, (int)d.algo, (int)d.proto);
     if (!fn) return POLAR_EUNSUPPORTED;
+    c->last = d;                      // the policy's decision (what the hook returned)
     if (c->is_virtual) {
         const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
     }
-    c->last = d;
+    c->last_nch = d.nchannels;        // what is launched
     if (count == 0 || c->nranks == 1) return POLAR_OK;
     if (cudaSetDevice(c->device) != cudaSuccess) return POLAR_ECUDA;
 
@@ -586,6 +588,13 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out) {
     if (!comm || !out) return POLAR_EINVAL;
     *out = comm->last;
+    return POLAR_OK;
+}
+
+polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint32_t* grid) {
+    if (!comm) return POLAR_EINVAL;
+    if (nchannels) *nchannels = comm->last_nch;
+    if (grid) *grid = comm->last_nch * (uint32_t)comm->nlocal;
     return POLAR_OK;
 }
 

@@ -85,6 +85,86 @@ __device__ __forceinline__ void geo_slice(const Geo& g, unsigned long long NP, u
 // from every rank, reduces in rank order, stores the result into every rank's
 // shard r; exit barrier.  NVLink bytes per rank: 2(n-1)/n * S.
 
+// Dynamic chunk loop of the zero-copy two-shot, specialised on the rank count:
+// N in {2,3,4} keeps U = 8/N packs per thread in flight (8 independent 16-B
+// loads, so small n does not starve the memory system); N = 0 is the generic
+// predicated path (one pack x n ranks; n >= 5 already has >= 5 loads in flight).
+// Templating the WHOLE loop (not just its body) keeps each variant's pointers
+// out of the others' live ranges (the body-level switch spilled at 128 regs).
+struct TwoShotGeo {
+    unsigned long long s0, s1, nbig, bigend, nchunks, nfull, wbase;
+    unsigned long long* work;
+};
+constexpr unsigned long long kTsBig = 2048, kTsSmall = 256;   // packs (32 KiB / 4 KiB per buffer)
+
+template <int DT, int OP, int N>
+__device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, const TwoShotGeo& g) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int NR = N ? N : kMaxRanks;
+    constexpr int U = (N >= 2 && N <= 4) ? 8 / N : 1;
+    const int n = w.n, tid = w.tid;
+    __shared__ unsigned long long s_next;
+    if (tid == 0) {
+        atomicMax(g.work, g.wbase);
+        s_next = atomicAdd(g.work, 1ull) - g.wbase;
+    }
+    __syncthreads();
+    unsigned long long k = s_next;
+    const uint4* src[NR];
+#pragma unroll
+    for (int p = 0; p < NR; ++p) src[p] = reinterpret_cast<const uint4*>(P.bufs[(N || p < n) ? p : 0]);
+    const unsigned long long stride = (unsigned long long)blockDim.x;
+    while (k < g.nchunks) {
+        __syncthreads();                                         // everyone has read s_next
+        if (tid == 0) s_next = atomicAdd(g.work, 1ull) - g.wbase;   // prefetch the next grab
+        const unsigned long long a = g.s0 + (k < g.nbig ? k * kTsBig : g.bigend + (k - g.nbig) * kTsSmall);
+        unsigned long long b = a + (k < g.nbig ? kTsBig : kTsSmall);
+        if (b > g.s1) b = g.s1;
+        if (b <= g.nfull) {
+            // fast path: full, 16-B aligned packs
+#pragma unroll 1
+            for (unsigned long long i0 = a + tid; i0 < b; i0 += U * stride) {
+                uint4 v[U][NR];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const unsigned long long i = i0 + u * stride;
+                    if (i < b) {
+#pragma unroll
+                        for (int p = 0; p < NR; ++p)
+                            if (N || p < n) v[u][p] = ld_cg(src[p] + i);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const unsigned long long i = i0 + u * stride;
+                    if (i < b) {
+                        Acc<DT> acc;
+                        acc_init<DT>(acc, v[u][0]);
+#pragma unroll
+                        for (int p = 1; p < NR; ++p)
+                            if (N || p < n) acc_add<DT, OP>(acc, v[u][p]);
+                        const uint4 out = acc_fin<DT>(acc);
+#pragma unroll
+                        for (int p = 0; p < NR; ++p)
+                            if (N || p < n) const_cast<uint4*>(src[p])[i] = out;
+                    }
+                }
+            }
+        } else {
+            // partial last pack / unaligned buffers: element-exact copies
+            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+                Acc<DT> acc;
+                acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0], i));
+                for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p], i));
+                const uint4 out = acc_fin<DT>(acc);
+                for (int p = 0; p < n; ++p) store_pack<ES>(P, P.bufs[p], i, out);
+            }
+        }
+        __syncthreads();                                         // chunk done, s_next visible
+        k = s_next;
+    }
+}
+
 template <int DT, int OP>
 __device__ void twoshot_simple(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
@@ -103,64 +183,23 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     // owner's scratch (ChanState[0].work = (epoch << 32) | next), so a slower
     // SM takes fewer chunks (static slices left a ~15 % loop-time spread,
     // measured with polar_comm_set_trace).  Big chunks first, then small ones
-    // for the last nch*kBig packs so the tail is balanced too.
+    // for the last nch*kTsBig packs so the tail is balanced too.
+    TwoShotGeo g;
     const unsigned long long NP = npacks<ES>(P);
-    unsigned long long s0, s1;
-    split_range(0, NP, n, w.r, s0, s1);
-    const unsigned long long L = s1 - s0;
-    constexpr unsigned long long kBig = 2048, kSmall = 256;   // packs (32 KiB / 4 KiB per buffer)
-    const unsigned long long tail = L < (unsigned long long)P.nch * kBig ? L : (unsigned long long)P.nch * kBig;
-    const unsigned long long nbig = (L - tail) / kBig;
-    const unsigned long long bigend = nbig * kBig;
-    const unsigned long long nchunks = nbig + (L - bigend + kSmall - 1) / kSmall;
-    const unsigned long long nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
-    unsigned long long* work = reinterpret_cast<unsigned long long*>(&chan_state(P, w.r, 0)->work);
-    const unsigned long long wbase = (unsigned long long)e << 32;
-    __shared__ unsigned long long s_next;
-    if (tid == 0) {
-        atomicMax(work, wbase);
-        s_next = atomicAdd(work, 1ull) - wbase;
-    }
-    __syncthreads();
-    unsigned long long k = s_next;
-    const uint4* src[kMaxRanks];
-#pragma unroll
-    for (int p = 0; p < kMaxRanks; ++p) src[p] = reinterpret_cast<const uint4*>(P.bufs[p < n ? p : 0]);
-    while (k < nchunks) {
-        __syncthreads();                                   // everyone has read s_next
-        if (tid == 0) s_next = atomicAdd(work, 1ull) - wbase;   // prefetch the next grab
-        const unsigned long long a = s0 + (k < nbig ? k * kBig : bigend + (k - nbig) * kSmall);
-        unsigned long long b = a + (k < nbig ? kBig : kSmall);
-        if (b > s1) b = s1;
-        if (b <= nfull) {
-            // fast path: full aligned packs, hoisted bases, 2n... loads in flight
-            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
-                uint4 v[kMaxRanks];
-#pragma unroll
-                for (int p = 0; p < kMaxRanks; ++p)
-                    if (p < n) v[p] = ld_cg(src[p] + i);
-                Acc<DT> acc;
-                acc_init<DT>(acc, v[0]);
-#pragma unroll
-                for (int p = 1; p < kMaxRanks; ++p)
-                    if (p < n) acc_add<DT, OP>(acc, v[p]);
-                const uint4 out = acc_fin<DT>(acc);
-#pragma unroll
-                for (int p = 0; p < kMaxRanks; ++p)
-                    if (p < n) const_cast<uint4*>(src[p])[i] = out;
-            }
-        } else {
-            // partial last pack / unaligned buffers: element-exact copies
-            for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
-                Acc<DT> acc;
-                acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0], i));
-                for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p], i));
-                const uint4 out = acc_fin<DT>(acc);
-                for (int p = 0; p < n; ++p) store_pack<ES>(P, P.bufs[p], i, out);
-            }
-        }
-        __syncthreads();                                   // chunk done, s_next visible
-        k = s_next;
+    split_range(0, NP, n, w.r, g.s0, g.s1);
+    const unsigned long long L = g.s1 - g.s0;
+    const unsigned long long tail = L < (unsigned long long)P.nch * kTsBig ? L : (unsigned long long)P.nch * kTsBig;
+    g.nbig = (L - tail) / kTsBig;
+    g.bigend = g.nbig * kTsBig;
+    g.nchunks = g.nbig + (L - g.bigend + kTsSmall - 1) / kTsSmall;
+    g.nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
+    g.work = reinterpret_cast<unsigned long long*>(&chan_state(P, w.r, 0)->work);
+    g.wbase = (unsigned long long)e << 32;
+    switch (n) {
+        case 2: twoshot_loop<DT, OP, 2>(P, w, g); break;
+        case 3: twoshot_loop<DT, OP, 3>(P, w, g); break;
+        case 4: twoshot_loop<DT, OP, 4>(P, w, g); break;
+        default: twoshot_loop<DT, OP, 0>(P, w, g); break;
     }
     __syncthreads();
     trace_point(P, 2);

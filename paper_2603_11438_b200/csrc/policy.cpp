@@ -29,7 +29,7 @@ constexpr uint64_t KiB = 1024, MiB = 1024 * 1024;
 const polar_policy_row kDefaultRows[] = {
     {POLAR_COLL_ALLREDUCE, 0, 64 * KiB, POLAR_ALGO_ONESHOT, POLAR_PROTO_LL, 4, 0},
     {POLAR_COLL_ALLREDUCE, 0, 1 * MiB, POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE, 8, 0},
-    {POLAR_COLL_ALLREDUCE, 0, ~uint64_t(0), POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE, 16, 0},
+    {POLAR_COLL_ALLREDUCE, 0, ~uint64_t(0), POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE, 32, 0},
 };
 constexpr uint32_t kNumDefault = sizeof(kDefaultRows) / sizeof(kDefaultRows[0]);
 

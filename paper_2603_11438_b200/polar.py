@@ -107,6 +107,7 @@ _sigs = {
     "polar_allreduce_host": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_comm_last_decision": (C.c_int, [_P, C.POINTER(Decision)]),
     "polar_comm_launches": (C.c_uint64, [_P]),
+    "polar_comm_launch_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "polar_comm_check": (C.c_int, [_P]),
     "polar_comm_set_trace": (C.c_int, [_P, _P, C.c_size_t]),
     "polar_bench_enqueue": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P, C.c_uint64,
@@ -335,6 +336,11 @@ class Comm:
         d = Decision()
         _check(lib.polar_comm_last_decision(self.h, C.byref(d)), "polar_comm_last_decision")
         return d
+
+    def launched_channels(self) -> int:
+        nch = C.c_uint32(0)
+        _check(lib.polar_comm_launch_info(self.h, C.byref(nch), None), "polar_comm_launch_info")
+        return nch.value
 
     def launches(self) -> int:
         return lib.polar_comm_launches(self.h)

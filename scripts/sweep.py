@@ -89,7 +89,7 @@ def main():
                 bus = size * 2 * (n - 1) / n / t / 1e9
                 hbm = 2 * n * size / t / 1e9
                 print(json.dumps({"n": n, "dtype": dt, "bytes": size, "algo": algo, "proto": proto,
-                                  "nch": comm.last_decision().nchannels, "us": round(t * 1e6, 2),
+                                  "nch": comm.launched_channels(), "us": round(t * 1e6, 2),
                                   "busbw_gbs": round(bus, 1), "min_hbm_gbs": round(hbm, 1)}), flush=True)
 
 

@@ -39,7 +39,7 @@ def main():
         comm.allreduce_forced(bufs, a.algo, a.proto, a.nch)
         e1.record()
         torch.cuda.synchronize()
-        nch = comm.last_decision().nchannels
+        nch = comm.launched_channels()
         t = tr.view(-1, 4)[: a.n * nch].cpu().double()
         base = t[:, 0].min()
         t = (t - base) / 1e3   # us
@@ -64,7 +64,7 @@ def main():
     comm.set_trace(tr2)
     comm.allreduce_forced(bufs, a.algo, a.proto, a.nch)
     torch.cuda.synchronize()
-    nch = comm.last_decision().nchannels
+    nch = comm.launched_channels()
     t1 = tr.view(-1, 4)[: a.n * nch].cpu().double()
     t2 = tr2.view(-1, 4)[: a.n * nch].cpu().double()
     print(json.dumps({"gap_us": round(float(t2[:, 0].min() - t1[:, 3].max()) / 1e3, 2),
