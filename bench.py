@@ -389,7 +389,7 @@ def time_nccl(args, buf, count, n, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="polar", choices=["polar", "reference"])
     ap.add_argument("--policy", default=os.environ.get("POLAR_POLICY", ""),

@@ -92,6 +92,8 @@ struct polar_comm_s {
     char* scratch[kMaxRanks] = {};       // rank p's scratch as addressable here
     std::vector<Registration> regs;
     std::vector<char*> ipc_mapped;       // to close at destroy
+    struct Opened { int peer; cudaIpcMemHandle_t h; char* base; };
+    std::vector<Opened> opened;          // IPC handles already opened (one open per allocation)
     std::vector<char*> virt_allocs;      // polar_mem_alloc on virtual comms
     int* err_host = nullptr;
     int* err_dev = nullptr;
@@ -267,11 +269,20 @@ polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks])
     if (c->ag(&mine, all.data(), sizeof(Msg), c->user) != 0) return POLAR_ESTATE;
     for (int p = 0; p < c->nranks; ++p) {
         if (p == c->rank0) { peer[p] = ptr; continue; }
-        void* m = nullptr;
-        cudaError_t e = cudaIpcOpenMemHandle(&m, all[p].h, cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) { (void)cudaGetLastError(); return POLAR_ECUDA; }
-        c->ipc_mapped.push_back(reinterpret_cast<char*>(m));
-        peer[p] = reinterpret_cast<char*>(m) + all[p].off;
+        // a peer allocation may back several registrations (caching allocators):
+        // open each IPC handle once and reuse the mapping
+        char* base_p = nullptr;
+        for (const auto& o : c->opened)
+            if (o.peer == p && std::memcmp(&o.h, &all[p].h, sizeof(cudaIpcMemHandle_t)) == 0) base_p = o.base;
+        if (!base_p) {
+            void* m = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&m, all[p].h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) { (void)cudaGetLastError(); return POLAR_ECUDA; }
+            base_p = reinterpret_cast<char*>(m);
+            c->ipc_mapped.push_back(base_p);
+            c->opened.push_back({p, all[p].h, base_p});
+        }
+        peer[p] = base_p + all[p].off;
     }
     return POLAR_OK;
 }

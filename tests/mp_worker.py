@@ -74,6 +74,16 @@ def main():
     comm.allreduce_forced(buf, "twoshot", "simple", 8)
     torch.cuda.synchronize()
     check("twoshot/simple/registered", buf, xs, "f32", "sum", True)
+    # two registrations inside one torch allocation (caching-allocator pattern):
+    # the second must reuse the first IPC mapping; zero-copy two-shot on a view
+    big = torch.empty(3 * count, dtype=torch.float32, device="cuda")
+    comm.register(big[:count])
+    view = big[count:2 * count]
+    comm.register(view)
+    view.copy_(torch.from_numpy(xs[rank]))
+    comm.allreduce_forced(view, "twoshot", "simple", 4)
+    torch.cuda.synchronize()
+    check("twoshot/simple/registered-view", view, xs, "f32", "sum", True)
     # policy-selected on a plain torch tensor (unregistered: bounce path if two-shot)
     t = to_device(xs[rank], "f32")
     comm.allreduce(t)
