@@ -108,6 +108,7 @@ struct polar_comm_s {
     unsigned long long* trace = nullptr; // diagnostic per-CTA timestamps
     bool coop = true;                    // virtual: cooperative launch (co-residency guaranteed)
     bool pdl = true;                     // programmatic dependent launch (POLAR_PDL=0 disables)
+    int tma_mode = 2;                    // two-shot Simple via TMA smem staging: 0 never, 1 always, 2 auto
     unsigned long long timeout_ns = 0;
     std::mutex mu;
 };
@@ -160,12 +161,13 @@ polar_status check_latched(polar_comm_s* c) {
     return c->latched;
 }
 
-polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int grid, cudaStream_t stream) {
+polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int grid, cudaStream_t stream,
+                          size_t smem = 0) {
     void* args[] = {&P};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(dev::kBlock);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
     unsigned n = 0;
@@ -217,7 +219,23 @@ polar_status alloc_common(polar_comm_s* c) {
     {
         const char* ev = std::getenv("POLAR_PDL");
         c->pdl = !(ev && ev[0] == '0');
+        // TMA-staged two-shot: POLAR_TWOSHOT_TMA=1 always, =0 never, unset = auto:
+        // virtual comms with n <= 2 and >= 64 MiB (the measured crossover: TMA 4.35
+        // vs LDG 4.13 TB/s at n=2/512 MiB; LDG ahead at n=8 and below 64 MiB, where
+        // the bulk pipeline fill costs ~8 us).  Real comms stay on LDG by default
+        // until bulk copies over peer-mapped NVLink memory are validated on a
+        // multi-GPU box (they are tested over same-GPU CUDA-IPC mappings).
+        const char* et = std::getenv("POLAR_TWOSHOT_TMA");
+        c->tma_mode = et ? (et[0] == '1' ? 1 : 0) : 2;
     }
+    // the two-shot Simple kernels may use up to tma_smem_bytes(8) of dynamic shared memory
+    const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
+    const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
+    for (int dt : dts)
+        for (int op : ops)
+            CU_TRY(cudaFuncSetAttribute(kernel_for(dt, op, POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dev::tma_smem_bytes(kMaxRanks)));
     c->timeout_ns = (unsigned long long)env_size("POLAR_TIMEOUT_MS", 20000) * 1000000ull;
     CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
     *c->err_host = 0;
@@ -353,6 +371,10 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     fill_params(c, P);
     P.nch = (int)d.nchannels;
     const int grid = c->nlocal * P.nch;
+    const bool ts_simple = d.algo == POLAR_ALGO_TWOSHOT && d.proto == POLAR_PROTO_SIMPLE;
+    const bool tma_auto = c->is_virtual && c->nranks <= 2 && count * (size_t)es >= (64u << 20);
+    P.tma = (ts_simple && (c->tma_mode == 1 || (c->tma_mode == 2 && tma_auto))) ? 1 : 0;
+    const size_t smem = P.tma ? dev::tma_smem_bytes(c->nranks) : 0;
     const size_t bytes = count * (size_t)es;
 
     if (c->is_virtual) {
@@ -363,7 +385,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         }
         P.vec = vec;
         P.count = count;
-        return launch_kernel(c, fn, P, grid, stream);
+        return launch_kernel(c, fn, P, grid, stream, smem);
     }
     char* mine = reinterpret_cast<char*>(bufs[0]);
     if (d.algo != POLAR_ALGO_TWOSHOT || d.proto != POLAR_PROTO_SIMPLE) {
@@ -371,7 +393,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         P.bufs[c->rank0] = mine;
         P.vec = reinterpret_cast<uintptr_t>(mine) % 16 == 0;
         P.count = count;
-        return launch_kernel(c, fn, P, grid, stream);
+        return launch_kernel(c, fn, P, grid, stream, smem);
     }
     // zero-copy two-shot needs every rank's buffer mapped
     const Registration* reg = find_reg(c, mine, bytes);
@@ -384,7 +406,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         }
         P.vec = vec;
         P.count = count;
-        return launch_kernel(c, fn, P, grid, stream);
+        return launch_kernel(c, fn, P, grid, stream, smem);
     }
     // unregistered: bounce through the symmetric scratch, chunk by chunk
     const size_t chunk_elems = std::max<size_t>(1, (c->L.bounce_bytes / es) & ~(size_t)7);
@@ -395,7 +417,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         char* src = mine + done * es;
         CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, stream));
         P.count = n;
-        st = launch_kernel(c, fn, P, grid, stream);
+        st = launch_kernel(c, fn, P, grid, stream, smem);
         if (st != POLAR_OK) return st;
         CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, stream));
     }

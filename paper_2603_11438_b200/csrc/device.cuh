@@ -42,6 +42,7 @@ struct Params {
     unsigned long long tree_off, tree_slot, treell_off, treell_slot;
     unsigned long long* trace;  // optional per-CTA timestamps (polar_comm_set_trace), else null
     int sys;                    // 1: peers are other GPUs (system-scope ordering); 0: one GPU (gpu scope)
+    int tma;                    // two-shot Simple: 1 = TMA bulk-copy staging through shared memory
 };
 
 
@@ -105,6 +106,60 @@ __device__ __forceinline__ uint4 ld_ll(const uint4* p) {
                  : "memory");
     return v;
 }
+
+// ----------------------------------------------------- TMA bulk copies + mbarrier
+constexpr int kTmaStages = 6;                           // 5 stages in flight while one is reduced
+constexpr size_t kTmaStageBytes = 32 << 10;             // n tiles per stage, 32 KiB whatever n
+__host__ __device__ constexpr unsigned tma_tile_packs(int n) { return (unsigned)(kTmaStageBytes / 16 / n); }
+// dynamic shared memory of the TMA two-shot: stages + mbarriers + metadata
+__host__ __device__ constexpr size_t tma_smem_bytes(int /*n*/) {
+    return (size_t)kTmaStages * kTmaStageBytes + kTmaStages * (8 + 8 + 8 + 8) + 128;
+}
+
+// cp.async.bulk (SASS UBLKCP) moves whole tiles between global memory (local or
+// peer-mapped) and shared memory; completion of loads is tracked by an mbarrier
+// transaction count, stores by bulk async-groups.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // ------------------------------------------------------------------ errors
 

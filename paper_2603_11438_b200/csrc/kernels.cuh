@@ -165,6 +165,128 @@ __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, cons
     }
 }
 
+
+// TMA-staged variant of the zero-copy two-shot loop (Params.tma), warp
+// specialised.  Warp 0 / lane 0 is the producer: it grabs chunks from the same
+// per-owner counter, cuts them into (32 KiB / n)-per-rank tiles, issues one
+// cp.async.bulk load per rank into a shared-memory stage (its `full` mbarrier
+// counts the bytes), and once the consumers have released a stage (`empty`
+// mbarrier, one arrival per consumer warp) issues one bulk store per rank of
+// the reduced tile and reuses the stage after the stores have read it.  Warps
+// 1..15 reduce each stage in rank order from shared memory into the rank-0
+// slot.  kTmaStages stages of 32 KiB per CTA.  Only full 16-B packs go through
+// TMA; the partial last pack (if any) is finished with the slow path.
+template <int DT, int OP>
+__device__ void twoshot_tma(const Params& P, const Who& w, const TwoShotGeo& g) {
+    constexpr int ES = DType<DT>::ES;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int n = w.n, tid = w.tid;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nconsumer_warps = (int)(blockDim.x >> 5) - 1;
+    const unsigned tile_pk = tma_tile_packs(n);             // packs per rank per tile
+    const size_t tile_b = (size_t)tile_pk * 16;
+    unsigned char* data = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kTmaStages * kTmaStageBytes);
+    uint64_t* empty = full + kTmaStages;
+    unsigned long long* meta_off = reinterpret_cast<unsigned long long*>(empty + kTmaStages);
+    unsigned long long* meta_npk = meta_off + kTmaStages;
+    __shared__ unsigned long long s_tail_lo, s_tail_hi;   // slow-path remainder grabbed by this CTA
+    if (tid == 0) {
+        for (int st = 0; st < kTmaStages; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], (uint32_t)nconsumer_warps);
+        }
+        mbar_fence_init();
+        s_tail_lo = s_tail_hi = 0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------- producer
+            atomicMax(g.work, g.wbase);
+            unsigned long long pos = 0, fend = 0, tail_lo = 0, tail_hi = 0;
+            bool done = false;
+            // iteration t: drain tile d = t-(S-1) (wait for its reduction, issue its
+            // stores), then load tile t into stage t%S, whose previous tile t-S was
+            // drained one iteration ago: wait_group.read<1> lets the stores just
+            // issued stay in flight while guaranteeing that older ones have read.
+            for (unsigned t = 0;; ++t) {
+                const int st = (int)(t % kTmaStages);
+                if (t >= (unsigned)(kTmaStages - 1)) {
+                    const unsigned d = t - (kTmaStages - 1);
+                    const int sd = (int)(d % kTmaStages);
+                    while (!mbar_try_wait(&empty[sd], (d / kTmaStages) & 1)) {}
+                    const unsigned long long npk = meta_npk[sd], off = meta_off[sd];
+                    if (npk == 0) break;                    // end marker reached: everything stored
+                    const void* res = data + (size_t)sd * kTmaStageBytes;
+                    for (int p = 0; p < n; ++p) bulk_store(P.bufs[p] + off * 16, res, (uint32_t)(npk * 16));
+                    bulk_commit();
+                }
+                if (t >= (unsigned)kTmaStages) bulk_wait_read<1>();   // tile t-S's stores have read stage st
+                // next tile into stage st (or the end marker)
+                while (!done && pos >= fend) {
+                    const unsigned long long k = atomicAdd(g.work, 1ull) - g.wbase;
+                    if (k >= g.nchunks) { done = true; break; }
+                    const unsigned long long a = g.s0 + (k < g.nbig ? k * kTsBig : g.bigend + (k - g.nbig) * kTsSmall);
+                    unsigned long long b = a + (k < g.nbig ? kTsBig : kTsSmall);
+                    if (b > g.s1) b = g.s1;
+                    pos = a;
+                    fend = b < g.nfull ? b : (a > g.nfull ? a : g.nfull);
+                    if (b > fend) { tail_lo = fend; tail_hi = b; }
+                }
+                if (done) {
+                    meta_npk[st] = 0;
+                    mbar_arrive(&full[st]);                 // end marker
+                    continue;
+                }
+                const unsigned long long npk = (fend - pos) < tile_pk ? (fend - pos) : tile_pk;
+                meta_off[st] = pos;
+                meta_npk[st] = npk;
+                mbar_arrive_expect_tx(&full[st], (uint32_t)(n * npk * 16));
+                for (int p = 0; p < n; ++p)
+                    bulk_load(data + (size_t)st * kTmaStageBytes + p * tile_b, P.bufs[p] + pos * 16,
+                              (uint32_t)(npk * 16), &full[st]);
+                pos += npk;
+            }
+            bulk_wait_all();             // every result tile written
+            fence_proxy_async_global();  // async-proxy writes ordered before the generic exit flag
+            s_tail_lo = tail_lo;
+            s_tail_hi = tail_hi;
+        }
+    } else {
+        // ---------------------------------------------------------- consumers
+        const unsigned ctid = (unsigned)(tid - 32), cthreads = blockDim.x - 32;
+        for (unsigned t = 0;; ++t) {
+            const int st = (int)(t % kTmaStages);
+            while (!mbar_try_wait(&full[st], (t / kTmaStages) & 1)) {}
+            const unsigned long long npk = meta_npk[st];
+            if (npk != 0) {
+                uint4* tile0 = reinterpret_cast<uint4*>(data + (size_t)st * kTmaStageBytes);
+                for (unsigned j = ctid; j < npk; j += cthreads) {
+                    Acc<DT> acc;
+                    acc_init<DT>(acc, tile0[j]);
+                    for (int p = 1; p < n; ++p)
+                        acc_add<DT, OP>(acc, reinterpret_cast<const uint4*>(data + (size_t)st * kTmaStageBytes + p * tile_b)[j]);
+                    tile0[j] = acc_fin<DT>(acc);
+                }
+                fence_proxy_async_smem();   // my smem writes -> visible to the bulk store
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (npk == 0) break;
+        }
+    }
+    __syncthreads();
+    // slow-path remainder (the partial last pack) of a chunk this CTA grabbed
+    for (unsigned long long i = s_tail_lo + tid; i < s_tail_hi; i += blockDim.x) {
+        Acc<DT> acc;
+        acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0], i));
+        for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p], i));
+        const uint4 out = acc_fin<DT>(acc);
+        for (int p = 0; p < n; ++p) store_pack<ES>(P, P.bufs[p], i, out);
+    }
+}
+
 template <int DT, int OP>
 __device__ void twoshot_simple(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
@@ -195,7 +317,9 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     g.nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
     g.work = reinterpret_cast<unsigned long long*>(&chan_state(P, w.r, 0)->work);
     g.wbase = (unsigned long long)e << 32;
-    switch (n) {
+    if (P.tma && P.vec) {
+        twoshot_tma<DT, OP>(P, w, g);
+    } else switch (n) {
         case 2: twoshot_loop<DT, OP, 2>(P, w, g); break;
         case 3: twoshot_loop<DT, OP, 3>(P, w, g); break;
         case 4: twoshot_loop<DT, OP, 4>(P, w, g); break;

@@ -28,10 +28,12 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
-def test_multiprocess_ipc_all_algorithms(tmp_path, nranks):
+@pytest.mark.parametrize("nranks,tma", [(2, "0"), (3, "0"), (2, "1")])
+def test_multiprocess_ipc_all_algorithms(tmp_path, nranks, tma):
+    """tma=1: the TMA-staged two-shot (cp.async.bulk) on CUDA-IPC-mapped peer memory."""
     out = tmp_path / "mp.json"
     env = dict(os.environ)
+    env["POLAR_TWOSHOT_TMA"] = tma
     env.setdefault("POLAR_TIMEOUT_MS", "60000")
     env["POLAR_BOUNCE"] = str(1 << 20)   # small bounce buffer: exercise the chunked bounce path
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",

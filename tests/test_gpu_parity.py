@@ -168,3 +168,40 @@ def test_default_policy_bench_size_sampled():
         for t in ts:
             got = to_host(t[lo:hi], "f32")
             assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), (lo, hi)
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_twoshot_tma_forced(n, monkeypatch):
+    """The TMA-staged two-shot (cp.async.bulk + mbarrier pipeline), forced on a
+    dedicated comm: every dtype/op, ragged sizes spanning many tiles and chunks,
+    the partial last pack, and an unaligned buffer (falls back to the LDG path)."""
+    monkeypatch.setenv("POLAR_TWOSHOT_TMA", "1")
+    c = L.Comm.virtual(n, 0)
+    try:
+        for dtype in synth.DTYPES:
+            for op in ("sum", "max"):
+                for count, nch, off in ((1, 1, 0), (4097, 3, 0), (300_001, 8, 0), (1_234_567, 32, 0), (5000, 2, 1)):
+                    xs = synth.gen_ranks(dtype, count, n, cfg=12, dist=default_dist(dtype))
+                    ts = [to_device(x, dtype, off) for x in xs]
+                    c.allreduce_forced(ts, "twoshot", "simple", nch, op=op)
+                    torch.cuda.synchronize()
+                    c.check()
+                    check_result([to_host(t, dtype) for t in ts], xs, dtype, op, "twoshot", n)
+    finally:
+        c.destroy()
+
+
+def test_twoshot_tma_auto_large_n2():
+    """Auto selection takes the TMA path for n = 2 and >= 64 MiB: sampled parity."""
+    from oracle import allreduce as orc
+    n, count = 2, (96 << 20) // 4 + 5
+    xs = synth.gen_ranks("f32", count, n, cfg=13, dist="unif")
+    c = comm(n)
+    ts = [to_device(x, "f32") for x in xs]
+    c.allreduce_forced(ts, "twoshot", "simple", 32)
+    torch.cuda.synchronize()
+    c.check()
+    for lo, hi in ((0, 8192), (count // 2, count // 2 + 8192), (count - 9000, count)):
+        exp = orc.allreduce([x[lo:hi] for x in xs], "f32", "sum")
+        for t in ts:
+            assert np.array_equal(to_host(t[lo:hi], "f32").view(np.uint32), exp.view(np.uint32))
