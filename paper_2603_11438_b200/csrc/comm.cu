@@ -108,6 +108,7 @@ struct polar_comm_s {
     unsigned long long* trace = nullptr; // diagnostic per-CTA timestamps
     bool coop = true;                    // virtual: cooperative launch (co-residency guaranteed)
     bool pdl = true;                     // programmatic dependent launch (POLAR_PDL=0 disables)
+    unsigned jitter_ns = 0;              // fault injection (POLAR_JITTER_NS)
     int tma_mode = 2;                    // two-shot Simple via TMA smem staging: 0 never, 1 always, 2 auto
     unsigned long long timeout_ns = 0;
     std::mutex mu;
@@ -152,6 +153,7 @@ void fill_params(const polar_comm_s* c, dev::Params& P) {
     P.treell_off = L.treell_off; P.treell_slot = L.treell_slot;
     P.trace = c->trace;
     P.sys = c->is_virtual ? 0 : 1;
+    P.jitter_ns = c->jitter_ns;
 }
 
 polar_status check_latched(polar_comm_s* c) {
@@ -225,6 +227,7 @@ polar_status alloc_common(polar_comm_s* c) {
         // the bulk pipeline fill costs ~8 us).  Real comms stay on LDG by default
         // until bulk copies over peer-mapped NVLink memory are validated on a
         // multi-GPU box (they are tested over same-GPU CUDA-IPC mappings).
+        c->jitter_ns = (unsigned)env_size("POLAR_JITTER_NS", 0);
         const char* et = std::getenv("POLAR_TWOSHOT_TMA");
         c->tma_mode = et ? (et[0] == '1' ? 1 : 0) : 2;
     }

@@ -43,6 +43,8 @@ struct Params {
     unsigned long long* trace;  // optional per-CTA timestamps (polar_comm_set_trace), else null
     int sys;                    // 1: peers are other GPUs (system-scope ordering); 0: one GPU (gpu scope)
     int tma;                    // two-shot Simple: 1 = TMA bulk-copy staging through shared memory
+    unsigned jitter_ns;         // fault injection: random __nanosleep (< jitter_ns) before 1/8 of all
+                                // signal and LL stores (POLAR_JITTER_NS; 0 = off)
 };
 
 
@@ -160,6 +162,17 @@ template <int N> __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Fault injection: delay a random 1/8 of the signalling stores so
+// that every protocol is exercised under skewed arrival orders.
+__device__ __forceinline__ void jitter(const Params& P) {
+    if (P.jitter_ns == 0) return;
+    uint32_t x = (uint32_t)globaltimer() * 2654435761u ^ (threadIdx.x * 40503u) ^ (blockIdx.x * 2246822519u);
+    x ^= x >> 15;
+    x *= 2246822519u;
+    x ^= x >> 13;
+    if ((x & 7u) == 0) __nanosleep(x % P.jitter_ns);
+}
 
 // ------------------------------------------------------------------ errors
 

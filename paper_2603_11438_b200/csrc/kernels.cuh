@@ -294,7 +294,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e = st->epoch + 1;
     trace_point(P, 0);
-    if (tid < n) st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
+    if (tid < n) jitter(P), st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
     bool ok = true;
     if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
     if (!__syncthreads_and(ok)) return;
@@ -329,7 +329,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     trace_point(P, 2);
     if (tid < n) {
         fence_acq_rel(P.sys);
-        st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
+        jitter(P), st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
     }
     ok = true;
     if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
@@ -375,8 +375,8 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
             for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
                 const uint4 v = load_pack<ES>(P, mine, i);
                 uint4* l = dst + 2 * (i - lo);
-                st_ll(l, v.x, v.y, f);
-                st_ll(l + 1, v.z, v.w, f);
+                jitter(P), st_ll(l, v.x, v.y, f);
+                jitter(P), st_ll(l + 1, v.z, v.w, f);
             }
         }
         // reduce my part in rank order, keep it and push it to every rank
@@ -402,8 +402,8 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
             for (int p = 0; p < n; ++p) {
                 if (p == w.r) continue;
                 uint4* l = tsll_ag(P, p, par, w.r) + 2 * (off + i - lo);
-                st_ll(l, out.x, out.y, f);
-                st_ll(l + 1, out.z, out.w, f);
+                jitter(P), st_ll(l, out.x, out.y, f);
+                jitter(P), st_ll(l + 1, out.z, out.w, f);
             }
         }
         // AG receive: results of every other owner
@@ -459,7 +459,7 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
         __syncthreads();
         if (tid < n && tid != w.r) {
             fence_acq_rel(P.sys);
-            st_relaxed(flag_ptr(P, tid, F_OS, w.c, w.r), e, P.sys);
+            jitter(P), st_relaxed(flag_ptr(P, tid, F_OS, w.c, w.r), e, P.sys);
         }
         bool ok = true;
         if (tid < n && tid != w.r) ok = wait_geq(P, flag_ptr(P, w.r, F_OS, w.c, tid), e);
@@ -501,8 +501,8 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
             for (int p = 0; p < n; ++p) {
                 if (p == w.r) continue;
                 uint4* l = osll_slot(P, p, par, w.r) + 2 * (off + i - lo);
-                st_ll(l, v.x, v.y, f);
-                st_ll(l + 1, v.z, v.w, f);
+                jitter(P), st_ll(l, v.x, v.y, f);
+                jitter(P), st_ll(l + 1, v.z, v.w, f);
             }
         }
         for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
@@ -540,7 +540,9 @@ template <int PROTO> struct Fifo;
 template <> struct Fifo<POLAR_PROTO_SIMPLE> {
     // wire packs per slot for `wp` 16-B packs per element-pack
     static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 16; }
-    static __device__ __forceinline__ void put(uint4* slot, unsigned long long j, uint4 v, uint32_t) { st_plain(slot + j, v); }
+    static __device__ __forceinline__ void put(const Params&, uint4* slot, unsigned long long j, uint4 v, uint32_t) {
+        st_plain(slot + j, v);
+    }
     static __device__ __forceinline__ bool get(const Params&, const uint4* slot, unsigned long long j, uint32_t, uint4& v) {
         v = ld_cg(slot + j);
         return true;
@@ -548,9 +550,9 @@ template <> struct Fifo<POLAR_PROTO_SIMPLE> {
 };
 template <> struct Fifo<POLAR_PROTO_LL> {
     static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 32; }
-    static __device__ __forceinline__ void put(uint4* slot, unsigned long long j, uint4 v, uint32_t f) {
-        st_ll(slot + 2 * j, v.x, v.y, f);
-        st_ll(slot + 2 * j + 1, v.z, v.w, f);
+    static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long j, uint4 v, uint32_t f) {
+        jitter(P), st_ll(slot + 2 * j, v.x, v.y, f);
+        jitter(P), st_ll(slot + 2 * j + 1, v.z, v.w, f);
     }
     static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long j, uint32_t f, uint4& v) {
         uint4 l0, l1;
@@ -621,7 +623,7 @@ __device__ void ring(const Params& P, const Who& w) {
                     Acc<DT> acc;
                     acc_init<DT>(acc, load_pack<ES>(P, mine, i));
 #pragma unroll
-                    for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+                    for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
                 } else if (s < n) {
                     Acc<DT> acc;
 #pragma unroll
@@ -630,27 +632,27 @@ __device__ void ring(const Params& P, const Who& w) {
                     acc_add<DT, OP>(acc, load_pack<ES>(P, mine, i));
                     if (s < n - 1) {
 #pragma unroll
-                        for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+                        for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
                     } else {
                         const uint4 out = acc_fin<DT>(acc);
                         store_pack<ES>(P, mine, i, out);
-                        F::put(dst, j, out, fout);
+                        F::put(P, dst, j, out, fout);
                     }
                 } else {
                     uint4 v;
                     ok = F::get(P, src, j, fin, v);
                     if (!ok) break;
                     store_pack<ES>(P, mine, i, v);
-                    if (do_send) F::put(dst, j, v, fout);
+                    if (do_send) F::put(P, dst, j, v, fout);
                 }
             }
             if (!__syncthreads_and(ok)) return;
             if (tid == 0) {
                 if (do_send && PROTO == POLAR_PROTO_SIMPLE) {
                     fence_acq_rel(P.sys);
-                    st_relaxed(tail_out, sent + 1, P.sys);
+                    jitter(P), st_relaxed(tail_out, sent + 1, P.sys);
                 }
-                if (do_recv) st_relaxed(head_out, recvd + 1, P.sys);
+                if (do_recv) jitter(P), st_relaxed(head_out, recvd + 1, P.sys);
             }
             if (do_send) ++sent;
             if (do_recv) ++recvd;
@@ -741,16 +743,16 @@ __device__ void tree(const Params& P, const Who& w) {
                 store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
             } else {
 #pragma unroll
-                for (int q = 0; q < AW; ++q) F::put(dst, j * AW + q, acc.w[q], fout);
+                for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
             }
         }
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (!root && PROTO == POLAR_PROTO_SIMPLE) {
                 fence_acq_rel(P.sys);
-                st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1, P.sys);
+                jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1, P.sys);
             }
-            for (int k = 0; k < nchild; ++k) st_relaxed(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1, P.sys);
+            for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1, P.sys);
         }
         if (!root) ++usent;
         for (int k = 0; k < nchild; ++k) ++urecv[k];
@@ -778,15 +780,15 @@ __device__ void tree(const Params& P, const Who& w) {
                 if (!ok) break;
                 store_pack<ES>(P, mine, i, v);
             }
-            for (int k = 0; k < nchild; ++k) F::put(tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
+            for (int k = 0; k < nchild; ++k) F::put(P, tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
         }
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (PROTO == POLAR_PROTO_SIMPLE && nchild) {
                 fence_acq_rel(P.sys);
-                for (int k = 0; k < nchild; ++k) st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1, P.sys);
+                for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1, P.sys);
             }
-            if (!root) st_relaxed(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1, P.sys);
+            if (!root) jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1, P.sys);
         }
         if (nchild) ++dsent;
         if (!root) ++drecv;
