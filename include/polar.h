@@ -72,13 +72,21 @@ typedef struct {
 } polar_ctx;
 
 /* Tuner outputs ("writes algorithm, protocol, and channel count")
- * plus the policy generation that produced them. 16 B. */
+ * plus the policy generation that produced them and the
+ * matching row's flags. 24 B. */
 typedef struct {
-    uint32_t algo;        /* POLAR_ALGO_*                      */
-    uint32_t proto;       /* POLAR_PROTO_*                     */
-    uint32_t nchannels;   /* 1..POLAR_MAXCH                    */
-    uint32_t generation;  /* active policy generation at decide */
+    uint32_t algo;        /* POLAR_ALGO_*                                          */
+    uint32_t proto;       /* POLAR_PROTO_*                                         */
+    uint32_t nchannels;   /* 1..POLAR_MAXCH (with POLAR_ROW_ADAPTIVE_NCH: the cap) */
+    uint32_t generation;  /* active policy generation at decide                    */
+    uint32_t flags;       /* POLAR_ROW_* of the matching row (0 if none / default)  */
+    uint32_t _pad;
 } polar_decision;
+
+/* Row flags.  POLAR_ROW_ADAPTIVE_NCH: the channel count is chosen per call by the
+ * comm's profiler->tuner closed loop (polar_adaptive_*; PAPER.md L311-351,
+ * L597-611), between the controller's c_min and this row's nchannels (the cap). */
+#define POLAR_ROW_ADAPTIVE_NCH 0x1u
 
 /* One policy row. 32 B.  A policy is an ordered list of rows; the first row with
  * coll == ctx.coll, nranks in {0 (any), ctx.nranks} and ctx.bytes <= max_bytes
@@ -92,7 +100,7 @@ typedef struct {
     uint32_t algo;        /* POLAR_ALGO_* or POLAR_UNSET            */
     uint32_t proto;       /* POLAR_PROTO_* or POLAR_UNSET           */
     uint32_t nchannels;   /* 0 = UNSET; any other u32 is clamped    */
-    uint32_t _pad;        /* must be 0                              */
+    uint32_t flags;       /* POLAR_ROW_* bits; others must be 0     */
 } polar_policy_row;
 
 /* Host all-gather used ONLY at comm init / registration: gathers bytes_per_rank
@@ -105,7 +113,7 @@ typedef struct polar_comm_s* polar_comm_t;   /* opaque; owned by the library */
 
 /* Atomically replace the process-global policy (§4 "atomic
  * compare-and-swap on the pointer").  The rows are COPIED.
- * Validation: nrows <= 64; known enums; nranks <= 8; _pad == 0; rows of one
+ * Validation: nrows <= 64; known enums; nranks <= 8; only known flag bits; rows of one
  * (coll, nranks) group strictly ascending in max_bytes -> else POLAR_EINVAL;
  * NVLS or LL128 -> POLAR_EUNSUPPORTED.  On any rejection the active policy and
  * its generation are unchanged ("the old policy continues").
@@ -265,6 +273,53 @@ polar_status polar_comm_check(polar_comm_t comm);
  * dependent points; two-shot: start, after entry barrier, loop end, exit).
  * bytes must hold nlocal*32*4 u64.  NULL disables. */
 polar_status polar_comm_set_trace(polar_comm_t comm, void* dev_buf, size_t bytes);
+
+/* ------------------------------------------- profiler -> tuner closed loop (f3) */
+
+/* The paper's composability case study (§5.3; Listing 1
+ * L311-351) rebuilt without eBPF maps: every AllReduce kernel writes its device
+ * duration (%globaltimer, CTA 0) into a host-mapped telemetry ring (the
+ * "profiler"); every `period` calls the comm's controller folds the completed
+ * samples of the window into a mean latency m (real comms: the max over ranks,
+ * gathered through the bootstrap all-gather so every rank picks the same count)
+ * and updates the channel count c used by rows flagged POLAR_ROW_ADAPTIVE_NCH
+ * (R15):
+ *     ref = ref[c] if known else ref[c-1];
+ *     if ref known and m > contention_factor * ref:   c = c_min   (back off)
+ *     else: ref[c] = m; c = min(c + 1, cap)                       (ramp)
+ * A window without samples (profiler off) changes nothing: c stays at c_min. */
+typedef struct {
+    uint32_t enabled;           /* 1: telemetry recorded and consumed ("profiler loaded") */
+    uint32_t period;            /* calls per window (>= 1)                               */
+    uint32_t c_min;             /* starting / back-off channel count (>= 1)              */
+    uint32_t _pad;
+    double contention_factor;   /* > 1                                                   */
+    double latency_scale;       /* multiplies measured latencies (contention injection,   *
+                                 * SPEC.md L366-368); 1.0 in production                   */
+} polar_adaptive_params;
+
+typedef struct {
+    uint32_t channels;          /* current c                              */
+    uint32_t contended;         /* last window judged contended           */
+    uint64_t windows;           /* windows closed                         */
+    uint64_t samples;           /* telemetry samples consumed             */
+    double last_mean_ns;        /* mean latency of the last closed window */
+} polar_adaptive_state;
+
+/* Configure (and reset) a comm's closed loop.  Collective for real comms (same
+ * params on every rank).  Default: enabled=0, period=1000, c_min=2, factor=4, scale=1. */
+polar_status polar_adaptive_config(polar_comm_t comm, const polar_adaptive_params* params);
+polar_status polar_adaptive_get_state(polar_comm_t comm, polar_adaptive_state* out);
+
+/* Change only latency_scale (contention injection) without resetting the state. */
+polar_status polar_adaptive_inject(polar_comm_t comm, double latency_scale);
+
+/* Pure host simulation of the controller rule above (no comm, no GPU): window w
+ * is observed at the current c and its mean is lat[w * 33 + c] ns (a table over
+ * channel counts 0..32 per window; NaN or <= 0 = no samples in that window).
+ * channels_out[w] = c after window w.  Used to pin the rule against the oracle. */
+polar_status polar_adaptive_simulate(const polar_adaptive_params* params, uint32_t cap, const double* lat,
+                                     uint32_t nwindows, uint32_t* channels_out);
 
 const char* polar_status_string(polar_status s);
 

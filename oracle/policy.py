@@ -16,7 +16,7 @@ Follows, step by step:
   upper bounds; the key is the total message bytes (R6).
 
 A policy here is DATA: an ordered list of rows
-``(coll, nranks, max_bytes, algo, proto, nchannels)``; the first row whose
+``(coll, nranks, max_bytes, algo, proto, nchannels[, flags])``; the first row whose
 ``coll`` equals the context's, whose ``nranks`` is 0 (any) or equal, and whose
 ``max_bytes`` >= the message bytes, wins.
 
@@ -37,6 +37,7 @@ COLL_ALLREDUCE, COLL_ALLGATHER, COLL_BROADCAST, COLL_REDUCESCATTER = 0, 1, 2, 3
 TREE, RING, NVLS, ONESHOT, TWOSHOT = 0, 1, 2, 3, 4
 LL, LL128, SIMPLE = 0, 1, 2
 UNSET = 0xFFFFFFFF
+ROW_ADAPTIVE_NCH = 0x1   # row flag: channels from the closed loop, nchannels = cap (R15)
 MAXCH = 32          # DESIGN.md R8
 MAXROWS = 64        # DESIGN.md "Policy table" bound
 MAXRANKS = 8
@@ -63,18 +64,18 @@ def _first_match(rows, coll: int, nranks: int, nbytes: int):
     return None
 
 
-def decide(rows, coll: int, nranks: int, nbytes: int):
-    """(algo, proto, nchannels) for one call, or None if the collective has no default.
+def decide_full(rows, coll: int, nranks: int, nbytes: int):
+    """(algo, proto, nchannels, flags) for one call, or None if the collective has no default.
 
     Per-field deferral: a matching row's UNSET algo/proto or 0 channels take the
     default table's value for the same context; then channels are clamped to
-    [1, MAXCH].
+    [1, MAXCH].  flags are the matching row's (0 if none matched).
     """
     d = _first_match(DEFAULT_ROWS, coll, nranks, nbytes)
     if d is None:
         return None
     m = _first_match(rows, coll, nranks, nbytes)
-    algo, proto, nch = d[3], d[4], d[5]
+    algo, proto, nch, flags = d[3], d[4], d[5], 0
     if m is not None:
         if m[3] != UNSET:
             algo = m[3]
@@ -82,8 +83,15 @@ def decide(rows, coll: int, nranks: int, nbytes: int):
             proto = m[4]
         if m[5] != 0:
             nch = m[5]
+        flags = m[6] if len(m) > 6 else 0
     nch = min(max(nch, 1), MAXCH)
-    return algo, proto, nch
+    return algo, proto, nch, flags
+
+
+def decide(rows, coll: int, nranks: int, nbytes: int):
+    """(algo, proto, nchannels) — decide_full without the flags."""
+    r = decide_full(rows, coll, nranks, nbytes)
+    return None if r is None else r[:3]
 
 
 def validate(rows) -> str:
@@ -97,7 +105,11 @@ def validate(rows) -> str:
         return "einval"
     unsupported = False
     last = {}
-    for (coll, nranks, max_bytes, algo, proto, nch) in rows:
+    for row in rows:
+        coll, nranks, max_bytes, algo, proto, nch = row[:6]
+        flags = row[6] if len(row) > 6 else 0
+        if flags & ~ROW_ADAPTIVE_NCH:
+            return "einval"
         if coll not in (COLL_ALLREDUCE, COLL_ALLGATHER, COLL_BROADCAST, COLL_REDUCESCATTER):
             return "einval"
         if nranks > MAXRANKS:

@@ -135,7 +135,7 @@ polar_status polar_bench_swap(uint32_t nthreads, uint64_t calls_per_thread, uint
     }
     // an invalid table (duplicate max_bytes): must be rejected without effect
     polar_policy_row badrows[2] = {{0, 0, 100, POLAR_ALGO_RING, POLAR_PROTO_LL, 1, 0},
-                                   {0, 0, 100, POLAR_ALGO_RING, POLAR_PROTO_LL, 1, 0}};
+                                   {0, 0, 100, POLAR_ALGO_RING, POLAR_PROTO_LL, 1, 0}};   // duplicate bound
     std::vector<uint64_t> swap_ns;
     swap_ns.reserve(nswaps);
     uint64_t rejected = 0, rejected_changed = 0, swaps = 0;

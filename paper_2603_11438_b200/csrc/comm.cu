@@ -109,6 +109,12 @@ struct polar_comm_s {
     bool coop = true;                    // virtual: cooperative launch (co-residency guaranteed)
     bool pdl = true;                     // programmatic dependent launch (POLAR_PDL=0 disables)
     unsigned jitter_ns = 0;              // fault injection (POLAR_JITTER_NS)
+    // profiler -> tuner closed loop (f3)
+    Adaptive ad;
+    TelEntry* tel_host = nullptr;        // host-mapped telemetry ring
+    TelEntry* tel_dev = nullptr;
+    unsigned long long tel_seq = 0;      // last launch sequence number handed out
+    unsigned long long tel_consumed = 0; // samples consumed up to (and including) this seq
     int tma_mode = 2;                    // two-shot Simple via TMA smem staging: 0 never, 1 always, 2 auto
     unsigned long long timeout_ns = 0;
     std::mutex mu;
@@ -243,6 +249,18 @@ polar_status alloc_common(polar_comm_s* c) {
     CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
     *c->err_host = 0;
     CU_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+    CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->tel_host), sizeof(TelEntry) * kTelRing, cudaHostAllocMapped));
+    std::memset(c->tel_host, 0, sizeof(TelEntry) * kTelRing);
+    CU_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->tel_dev), c->tel_host, 0));
+    {
+        polar_adaptive_params p{};
+        p.enabled = 0;
+        p.period = 1000;
+        p.c_min = 2;
+        p.contention_factor = 4.0;
+        p.latency_scale = 1.0;
+        adaptive_reset(c->ad, p);
+    }
     return POLAR_OK;
 }
 
@@ -264,6 +282,7 @@ void destroy_comm(polar_comm_s* c) {
     for (int p = 0; p < kMaxRanks; ++p)
         if (c->scratch_own[p]) cudaFree(c->scratch_own[p]);
     if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->tel_host) cudaFreeHost(c->tel_host);
     delete c;
 }
 
@@ -338,6 +357,46 @@ polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgat
     return POLAR_OK;
 }
 
+// Profiler side: fold every completed telemetry sample since the last drain
+// into the open window (latency_scale applied: contention injection).
+void adaptive_drain(polar_comm_s* c) {
+    while (c->tel_consumed < c->tel_seq) {
+        const unsigned long long want = c->tel_consumed + 1;
+        volatile TelEntry* e = c->tel_host + (want % kTelRing);
+        const unsigned long long seq = e->seq;
+        if (seq < want) break;                       // not completed yet (or never written)
+        if (seq == want) {
+            const double ns = (double)(e->t1 - e->t0) * c->ad.prm.latency_scale;
+            c->ad.win_sum += ns;
+            c->ad.win_cnt++;
+            c->ad.samples++;
+        }                                            // seq > want: overwritten by a later lap, lost
+        c->tel_consumed = want;
+    }
+}
+
+// Tuner side: at every `period`-th adaptive call (the same call index on every
+// rank) close the window.  Real comms gather the window means of all ranks
+// through the bootstrap all-gather and use their max, so every rank applies the
+// same rule to the same number and launches the same channel count.
+polar_status adaptive_tick(polar_comm_s* c, uint32_t cap) {
+    Adaptive& a = c->ad;
+    a.calls++;
+    if (a.calls % a.prm.period != 0) return POLAR_OK;
+    adaptive_drain(c);
+    double m = a.win_cnt ? a.win_sum / (double)a.win_cnt : 0.0;
+    if (!c->is_virtual && c->nranks > 1) {
+        std::vector<double> all(c->nranks, 0.0);
+        if (c->ag(&m, all.data(), sizeof(double), c->user) != 0) return POLAR_ESTATE;
+        m = 0.0;
+        for (double x : all) m = x > m ? x : m;
+    }
+    adaptive_close_window(a, m, cap);
+    a.win_sum = 0.0;
+    a.win_cnt = 0;
+    return POLAR_OK;
+}
+
 polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int dtype, int op,
                           const polar_decision* forced, cudaStream_t stream) {
     const int es = esize_of(dtype);
@@ -362,6 +421,12 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     const void* fn = kernel_for(dtype, op, (int)d.algo, (int)d.proto);
     if (!fn) return POLAR_EUNSUPPORTED;
     c->last = d;                      // the policy's decision (what the hook returned)
+    if ((d.flags & POLAR_ROW_ADAPTIVE_NCH) && count > 0 && c->nranks > 1) {
+        // closed loop: the row's nchannels is the cap, the controller picks c
+        st = adaptive_tick(c, d.nchannels);
+        if (st != POLAR_OK) return st;
+        d.nchannels = c->ad.c < d.nchannels ? c->ad.c : d.nchannels;
+    }
     if (c->is_virtual) {
         const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
@@ -374,6 +439,11 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     fill_params(c, P);
     P.nch = (int)d.nchannels;
     const int grid = c->nlocal * P.nch;
+    if (c->ad.prm.enabled) {
+        adaptive_drain(c);           // keep the ring from lapping between windows
+        P.tel = c->tel_dev;
+        P.seq = ++c->tel_seq;
+    }
     const bool ts_simple = d.algo == POLAR_ALGO_TWOSHOT && d.proto == POLAR_PROTO_SIMPLE;
     const bool tma_auto = c->is_virtual && c->nranks <= 2 && count * (size_t)es >= (64u << 20);
     P.tma = (ts_simple && (c->tma_mode == 1 || (c->tma_mode == 2 && tma_auto))) ? 1 : 0;
@@ -664,6 +734,32 @@ polar_status polar_bench_enqueue(polar_comm_t comm, void* const* bufs, size_t co
     CU_TRY(cudaStreamSynchronize(s));
     *ns_per_call = std::chrono::duration<double, std::nano>(t1 - t0).count() / (double)ncalls;
     return check_latched(comm);
+}
+
+polar_status polar_adaptive_config(polar_comm_t comm, const polar_adaptive_params* params) {
+    if (!comm || !params) return POLAR_EINVAL;
+    polar_status st = adaptive_validate(*params);
+    if (st != POLAR_OK) return st;
+    adaptive_reset(comm->ad, *params);
+    comm->tel_consumed = comm->tel_seq;   // forget samples of earlier calls
+    return POLAR_OK;
+}
+
+polar_status polar_adaptive_inject(polar_comm_t comm, double latency_scale) {
+    if (!comm || !(latency_scale > 0.0)) return POLAR_EINVAL;
+    comm->ad.prm.latency_scale = latency_scale;
+    return POLAR_OK;
+}
+
+polar_status polar_adaptive_get_state(polar_comm_t comm, polar_adaptive_state* out) {
+    if (!comm || !out) return POLAR_EINVAL;
+    adaptive_drain(comm);
+    out->channels = comm->ad.c;
+    out->contended = comm->ad.contended ? 1u : 0u;
+    out->windows = comm->ad.windows;
+    out->samples = comm->ad.samples;
+    out->last_mean_ns = comm->ad.last_mean;
+    return POLAR_OK;
 }
 
 const char* polar_version(void) { return "polar 0.1 sm_100a"; }

@@ -45,6 +45,8 @@ struct Params {
     int tma;                    // two-shot Simple: 1 = TMA bulk-copy staging through shared memory
     unsigned jitter_ns;         // fault injection: random __nanosleep (< jitter_ns) before 1/8 of all
                                 // signal and LL stores (POLAR_JITTER_NS; 0 = off)
+    TelEntry* tel;              // profiler telemetry ring (host-mapped), or null
+    unsigned long long seq;     // this launch's sequence number in the ring
 };
 
 

@@ -813,6 +813,9 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const Who w = who(P);
+    // profiler telemetry (f3): CTA 0 stamps the launch into the host-mapped ring
+    const bool tel = P.tel != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const unsigned long long tel_t0 = tel ? globaltimer() : 0;
     if constexpr (ALGO == POLAR_ALGO_TWOSHOT) {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) twoshot_simple<DT, OP>(P, w);
         else twoshot_ll<DT, OP>(P, w);
@@ -823,6 +826,13 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
         ring<DT, OP, PROTO>(P, w);
     } else {
         tree<DT, OP, PROTO>(P, w);
+    }
+    if (tel) {
+        volatile TelEntry* e = P.tel + (P.seq % kTelRing);
+        e->t0 = tel_t0;
+        e->t1 = globaltimer();
+        __threadfence_system();
+        e->seq = P.seq;
     }
 }
 

@@ -65,4 +65,28 @@ constexpr int kSteps = 4;  // FIFO depth (slots) per connection
 
 Layout make_layout(bool with_bounce);
 
+// ---------------------------------------------------- adaptive channels (f3)
+struct Adaptive {
+    polar_adaptive_params prm{};
+    uint32_t c = 2;               // current channel count
+    bool contended = false;
+    uint64_t windows = 0, samples = 0;
+    double last_mean = 0.0;
+    double ref[POLAR_MAXCH + 1] = {};   // last non-contended window mean per channel count (0 = unknown)
+    double win_sum = 0.0;         // samples of the open window
+    uint64_t win_cnt = 0;
+    uint64_t calls = 0;           // adaptive calls seen (window boundary every prm.period)
+};
+void adaptive_reset(Adaptive& a, const polar_adaptive_params& p);
+polar_status adaptive_validate(const polar_adaptive_params& p);
+void adaptive_close_window(Adaptive& a, double mean_ns, uint32_t cap);
+
+// telemetry ring entry written by the device (CTA 0 of each launch), host-mapped
+struct TelEntry {
+    unsigned long long seq;   // written last; == launch sequence number when t0/t1 are valid
+    unsigned long long t0, t1;
+    unsigned long long pad;
+};
+constexpr uint32_t kTelRing = 4096;
+
 }  // namespace polar

@@ -59,7 +59,7 @@ polar_status validate_rows(const polar_policy_row* rows, uint32_t nrows) {
         const polar_policy_row& r = rows[i];
         if (r.coll > POLAR_COLL_REDUCESCATTER) return POLAR_EINVAL;
         if (r.nranks > POLAR_MAXRANKS) return POLAR_EINVAL;
-        if (r._pad != 0) return POLAR_EINVAL;
+        if (r.flags & ~POLAR_ROW_ADAPTIVE_NCH) return POLAR_EINVAL;
         switch (r.algo) {
             case POLAR_ALGO_TREE: case POLAR_ALGO_RING: case POLAR_ALGO_ONESHOT:
             case POLAR_ALGO_TWOSHOT: case POLAR_UNSET: break;
@@ -86,12 +86,13 @@ polar_status decide_rows(const polar_policy_row* rows, uint32_t nrows, uint32_t 
     if (ctx->nranks < 1 || ctx->nranks > POLAR_MAXRANKS) return POLAR_EINVAL;
     const polar_policy_row* d = first_match(kDefaultRows, kNumDefault, ctx->coll, ctx->nranks, ctx->bytes);
     if (!d) return POLAR_EUNSUPPORTED;
-    uint32_t algo = d->algo, proto = d->proto, nch = d->nchannels;
+    uint32_t algo = d->algo, proto = d->proto, nch = d->nchannels, flags = 0;
     const polar_policy_row* m = first_match(rows, nrows, ctx->coll, ctx->nranks, ctx->bytes);
     if (m) {
         if (m->algo != POLAR_UNSET) algo = m->algo;
         if (m->proto != POLAR_UNSET) proto = m->proto;
         if (m->nchannels != 0) nch = m->nchannels;
+        flags = m->flags;
     }
     if (nch < 1) nch = 1;
     if (nch > POLAR_MAXCH) nch = POLAR_MAXCH;
@@ -99,6 +100,8 @@ polar_status decide_rows(const polar_policy_row* rows, uint32_t nrows, uint32_t 
     out->proto = proto;
     out->nchannels = nch;
     out->generation = generation;
+    out->flags = flags;
+    out->_pad = 0;
     return POLAR_OK;
 }
 

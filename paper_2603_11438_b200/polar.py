@@ -29,6 +29,7 @@ TREE, RING, NVLS, ONESHOT, TWOSHOT = 0, 1, 2, 3, 4
 LL, LL128, SIMPLE = 0, 1, 2
 UNSET = 0xFFFFFFFF
 MAXCH, MAXRANKS, MAXROWS = 32, 8, 64
+ROW_ADAPTIVE_NCH = 0x1
 
 DTYPE_CODES = {"i32": INT32, "i64": INT64, "f32": FLOAT32, "bf16": BFLOAT16}
 OP_CODES = {"sum": SUM, "max": MAX, "min": MIN}
@@ -52,7 +53,7 @@ class Ctx(C.Structure):
 
 class Decision(C.Structure):
     _fields_ = [("algo", C.c_uint32), ("proto", C.c_uint32), ("nchannels", C.c_uint32),
-                ("generation", C.c_uint32)]
+                ("generation", C.c_uint32), ("flags", C.c_uint32), ("_pad", C.c_uint32)]
 
     def as_tuple(self):
         return (self.algo, self.proto, self.nchannels)
@@ -64,7 +65,7 @@ class Decision(C.Structure):
 
 class PolicyRow(C.Structure):
     _fields_ = [("coll", C.c_uint32), ("nranks", C.c_uint32), ("max_bytes", C.c_uint64),
-                ("algo", C.c_uint32), ("proto", C.c_uint32), ("nchannels", C.c_uint32), ("_pad", C.c_uint32)]
+                ("algo", C.c_uint32), ("proto", C.c_uint32), ("nchannels", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class BenchStats(C.Structure):
@@ -78,6 +79,16 @@ class SwapStats(C.Structure):
                 ("nonmonotonic", C.c_uint64), ("swaps", C.c_uint64), ("rejected", C.c_uint64),
                 ("rejected_changed", C.c_uint64), ("swap_p50_ns", C.c_double), ("swap_p99_ns", C.c_double),
                 ("swap_max_ns", C.c_double), ("final_generation", C.c_uint32)]
+
+
+class AdaptiveParams(C.Structure):
+    _fields_ = [("enabled", C.c_uint32), ("period", C.c_uint32), ("c_min", C.c_uint32), ("_pad", C.c_uint32),
+                ("contention_factor", C.c_double), ("latency_scale", C.c_double)]
+
+
+class AdaptiveState(C.Structure):
+    _fields_ = [("channels", C.c_uint32), ("contended", C.c_uint32), ("windows", C.c_uint64),
+                ("samples", C.c_uint64), ("last_mean_ns", C.c_double)]
 
 
 AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -112,6 +123,11 @@ _sigs = {
     "polar_comm_set_trace": (C.c_int, [_P, _P, C.c_size_t]),
     "polar_bench_enqueue": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P, C.c_uint64,
                                       C.POINTER(C.c_double)]),
+    "polar_adaptive_config": (C.c_int, [_P, C.POINTER(AdaptiveParams)]),
+    "polar_adaptive_get_state": (C.c_int, [_P, C.POINTER(AdaptiveState)]),
+    "polar_adaptive_inject": (C.c_int, [_P, C.c_double]),
+    "polar_adaptive_simulate": (C.c_int, [C.POINTER(AdaptiveParams), C.c_uint32, C.POINTER(C.c_double), C.c_uint32,
+                                          C.POINTER(C.c_uint32)]),
     "polar_status_string": (C.c_char_p, [C.c_int]),
     "polar_version": (C.c_char_p, []),
 }
@@ -132,7 +148,7 @@ def _check(st, what):
 def rows_array(rows):
     arr = (PolicyRow * max(1, len(rows)))()
     for i, r in enumerate(rows):
-        arr[i] = PolicyRow(*[int(x) for x in r[:6]], 0)
+        arr[i] = PolicyRow(*[int(x) for x in r[:6]], int(r[6]) if len(r) > 6 else 0)
     return arr
 
 
@@ -164,7 +180,7 @@ def decide_batch(ctxs):
         a[i] = Ctx(COLL_ALLREDUCE, nr, b)
     out = (Decision * max(1, n))()
     _check(lib.polar_decide_batch(a, out, n), "polar_decide_batch")
-    return [(d.algo, d.proto, d.nchannels, d.generation) for d in out[:n]]
+    return [(d.algo, d.proto, d.nchannels, d.generation, d.flags) for d in out[:n]]
 
 
 def generation() -> int:
@@ -175,7 +191,8 @@ def get_policy():
     arr = (PolicyRow * MAXROWS)()
     n, g = C.c_uint32(0), C.c_uint32(0)
     _check(lib.polar_get_policy(arr, MAXROWS, C.byref(n), C.byref(g)), "polar_get_policy")
-    return [(r.coll, r.nranks, r.max_bytes, r.algo, r.proto, r.nchannels) for r in arr[:n.value]], g.value
+    return [(r.coll, r.nranks, r.max_bytes, r.algo, r.proto, r.nchannels) + ((r.flags,) if r.flags else ())
+            for r in arr[:n.value]], g.value
 
 
 def bench_decide(ctxs, nwarm=10_000, ncalls=400_000):
@@ -192,6 +209,22 @@ def bench_swap(rows_a, rows_b, nthreads=4, calls_per_thread=100_000, nswaps=1000
     _check(lib.polar_bench_swap(nthreads, calls_per_thread, nswaps, rows_array(rows_a), len(rows_a),
                                 rows_array(rows_b), len(rows_b), C.byref(s)), "polar_bench_swap")
     return {k: getattr(s, k) for k, _ in SwapStats._fields_}
+
+
+def adaptive_params(enabled=True, period=1000, c_min=2, contention_factor=4.0, latency_scale=1.0):
+    return AdaptiveParams(int(enabled), int(period), int(c_min), 0, float(contention_factor), float(latency_scale))
+
+
+def adaptive_simulate(params: AdaptiveParams, cap: int, lat_table):
+    """lat_table: list of windows, each a list of 33 latencies (index = channel count)."""
+    nw = len(lat_table)
+    flat = (C.c_double * max(1, nw * (MAXCH + 1)))()
+    for w, row in enumerate(lat_table):
+        for c in range(MAXCH + 1):
+            flat[w * (MAXCH + 1) + c] = float(row[c])
+    out = (C.c_uint32 * max(1, nw))()
+    _check(lib.polar_adaptive_simulate(C.byref(params), cap, flat, nw, out), "polar_adaptive_simulate")
+    return list(out[:nw])
 
 
 # ---------------------------------------------------------------- comms
@@ -336,6 +369,18 @@ class Comm:
         d = Decision()
         _check(lib.polar_comm_last_decision(self.h, C.byref(d)), "polar_comm_last_decision")
         return d
+
+    def adaptive_config(self, **kw):
+        p = adaptive_params(**kw)
+        _check(lib.polar_adaptive_config(self.h, C.byref(p)), "polar_adaptive_config")
+
+    def adaptive_inject(self, latency_scale: float):
+        _check(lib.polar_adaptive_inject(self.h, float(latency_scale)), "polar_adaptive_inject")
+
+    def adaptive_state(self):
+        s = AdaptiveState()
+        _check(lib.polar_adaptive_get_state(self.h, C.byref(s)), "polar_adaptive_get_state")
+        return {k: getattr(s, k) for k, _ in AdaptiveState._fields_}
 
     def launched_channels(self) -> int:
         nch = C.c_uint32(0)
