@@ -93,7 +93,11 @@ __device__ __forceinline__ uint4 ld_cg(const uint4* p) {
                  : "l"(p));
     return v;
 }
-__device__ __forceinline__ void st_plain(uint4* p, uint4 v) { *p = v; }
+// 16-B data store with an explicit global address space (STG.E.128; a plain
+// `*p = v` through the char* scratch/peer tables compiles to a generic ST.E.128)
+__device__ __forceinline__ void st_plain(uint4* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 
 // LL line: 16 B = {d0, flag, d1, flag}; written with one 16-B volatile store,
 // polled with one 16-B volatile load.
@@ -365,7 +369,7 @@ template <int ES> __device__ __forceinline__ uint4 load_pack(const Params& P, co
 }
 template <int ES> __device__ __forceinline__ void store_pack(const Params& P, char* base, unsigned long long idx, uint4 v) {
     int nv = pack_valid<ES>(P.count, idx);
-    if (P.vec && nv == 16 / ES) { reinterpret_cast<uint4*>(base)[idx] = v; return; }
+    if (P.vec && nv == 16 / ES) { st_plain(reinterpret_cast<uint4*>(base) + idx, v); return; }
     store_pack_slow<ES>(base, idx, v, nv);
 }
 

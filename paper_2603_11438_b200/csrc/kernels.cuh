@@ -146,7 +146,7 @@ __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, cons
                         const uint4 out = acc_fin<DT>(acc);
 #pragma unroll
                         for (int p = 0; p < NR; ++p)
-                            if (N || p < n) const_cast<uint4*>(src[p])[i] = out;
+                            if (N || p < n) st_plain(const_cast<uint4*>(src[p]) + i, out);
                     }
                 }
             }
