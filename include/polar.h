@@ -125,8 +125,9 @@ polar_status polar_set_policy(const polar_policy_row* rows, uint32_t nrows, uint
 
 /* The decision hook: pure, wait-free (one acquire load + a <=64-row scan), any
  * thread.  UNSET fields defer to the built-in default table (DESIGN.md "Default
- * table"); nchannels clamped to [1, POLAR_MAXCH].  coll != ALLREDUCE ->
- * POLAR_EUNSUPPORTED; NULL pointers or nranks outside 1..8 -> POLAR_EINVAL. */
+ * table"); nchannels clamped to [1, POLAR_MAXCH].  A collective without a
+ * default row (unknown coll) -> POLAR_EUNSUPPORTED; NULL pointers or nranks
+ * outside 1..8 -> POLAR_EINVAL. */
 polar_status polar_decide(const polar_ctx* ctx, polar_decision* out);
 
 /* Batched form for sweeps/tests: out[i] = decide(ctx[i]); stops at the first error. */
@@ -252,6 +253,33 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
  * is synchronised before and after the timed loop. */
 polar_status polar_bench_enqueue(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype,
                                  polar_op op, void* stream, uint64_t ncalls, double* ns_per_call);
+
+/* ------------------------------------------ other collectives through the hook (f4)
+ * ReduceScatter, AllGather and Broadcast are decided by the same hook
+ * (ctx.coll = POLAR_COLL_REDUCESCATTER / ALLGATHER / BROADCAST; ctx.bytes = the
+ * full buffer: recvcount*n*esize, sendcount*n*esize, count*esize) and run as ONE
+ * direct all-to-all step between an entry and an exit barrier (only algo
+ * ONESHOT + proto SIMPLE exist for them; any other decision -> EUNSUPPORTED).
+ * Semantics (NCCL's; oracle/collectives.py):
+ *   ReduceScatter: recv_r[i] = rank-ordered op over p of send_p[r*recvcount + i];
+ *                  in place allowed: recvbuf == sendbuf + rank*recvcount.
+ *   AllGather:     recv[p*sendcount + i] = send_p[i] on every rank;
+ *                  in place allowed: sendbuf == recvbuf + rank*sendcount.
+ *   Broadcast:     every rank's buf := root's buf.
+ * Real comms (nlocal = 1) must pass REGISTERED buffers for the memory peers
+ * access (RS: sendbuf, AG: recvbuf, BC: buf; same offsets on every rank) ->
+ * else POLAR_EINVAL.  The _v forms take nlocal pointers (virtual comms). */
+polar_status polar_reduce_scatter(polar_comm_t comm, const void* sendbuf, void* recvbuf, size_t recvcount,
+                                  polar_dtype dtype, polar_op op, void* stream);
+polar_status polar_reduce_scatter_v(polar_comm_t comm, void* const* sendbufs, void* const* recvbufs,
+                                    size_t recvcount, polar_dtype dtype, polar_op op, void* stream);
+polar_status polar_all_gather(polar_comm_t comm, const void* sendbuf, void* recvbuf, size_t sendcount,
+                              polar_dtype dtype, void* stream);
+polar_status polar_all_gather_v(polar_comm_t comm, void* const* sendbufs, void* const* recvbufs, size_t sendcount,
+                                polar_dtype dtype, void* stream);
+polar_status polar_broadcast(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, int root, void* stream);
+polar_status polar_broadcast_v(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype, int root,
+                               void* stream);
 
 /* Decision used by the most recent AllReduce on this comm. */
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);

@@ -53,6 +53,9 @@ DEFAULT_ROWS = [
     (COLL_ALLREDUCE, 0, 64 * KiB, ONESHOT, LL, 4),
     (COLL_ALLREDUCE, 0, 1 * MiB, ONESHOT, SIMPLE, 8),
     (COLL_ALLREDUCE, 0, U64_MAX, TWOSHOT, SIMPLE, 32),
+    (COLL_ALLGATHER, 0, U64_MAX, ONESHOT, SIMPLE, 32),
+    (COLL_BROADCAST, 0, U64_MAX, ONESHOT, SIMPLE, 32),
+    (COLL_REDUCESCATTER, 0, U64_MAX, ONESHOT, SIMPLE, 32),
 ]
 
 

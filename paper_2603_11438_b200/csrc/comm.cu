@@ -497,6 +497,84 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     return POLAR_OK;
 }
 
+// ReduceScatter (mode 0) / AllGather (1) / Broadcast (2): SURVEY f4.  count =
+// elements per block (RS recvcount, AG sendcount, BC count).  Real comms need
+// the peer-accessed buffers registered (RS: send, AG: recv, BC: buf).
+polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* const* recvs, size_t count, int dtype,
+                       int op, int root, cudaStream_t stream) {
+    const int es = esize_of(dtype);
+    if (!es || (mode == 0 && !op_ok(op))) return POLAR_EINVAL;
+    if (mode == 2 && (root < 0 || root >= c->nranks)) return POLAR_EINVAL;
+    if (count > 0 && (!sends || (mode != 2 && !recvs))) return POLAR_EINVAL;
+    for (int l = 0; l < c->nlocal && count > 0; ++l) {
+        if (!sends[l] || (reinterpret_cast<uintptr_t>(sends[l]) % es)) return POLAR_EINVAL;
+        if (mode != 2 && (!recvs[l] || (reinterpret_cast<uintptr_t>(recvs[l]) % es))) return POLAR_EINVAL;
+    }
+    polar_status st = check_latched(c);
+    if (st != POLAR_OK) return st;
+    static const uint32_t kColl[3] = {POLAR_COLL_REDUCESCATTER, POLAR_COLL_ALLGATHER, POLAR_COLL_BROADCAST};
+    const uint64_t bytes = (uint64_t)count * (uint64_t)es * (mode == 2 ? 1u : (uint64_t)c->nranks);
+    polar_ctx ctx{kColl[mode], (uint32_t)c->nranks, bytes};
+    polar_decision d;
+    st = polar_decide(&ctx, &d);
+    if (st != POLAR_OK) return st;
+    if (d.algo != POLAR_ALGO_ONESHOT || d.proto != POLAR_PROTO_SIMPLE) return POLAR_EUNSUPPORTED;
+    c->last = d;
+    if (c->is_virtual) {
+        const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
+        if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;
+    }
+    c->last_nch = d.nchannels;
+    if (count == 0) return POLAR_OK;
+    if (cudaSetDevice(c->device) != cudaSuccess) return POLAR_ECUDA;
+    const size_t blk = count * (size_t)es;
+    if (c->nranks == 1) {   // identity collectives: copy send -> recv where they differ
+        if (mode != 2 && sends[0] != recvs[0])
+            CU_TRY(cudaMemcpyAsync(recvs[0], sends[0], blk, cudaMemcpyDeviceToDevice, stream));
+        return POLAR_OK;
+    }
+    const void* fn = direct_kernel_for(dtype, mode, op);
+    if (!fn) return POLAR_EUNSUPPORTED;
+    dev::Params P;
+    fill_params(c, P);
+    P.nch = (int)d.nchannels;
+    P.count = count;
+    P.root = root;
+    const int grid = c->nlocal * P.nch;
+    bool vec = mode == 2 || (blk % 16) == 0;
+    auto aligned = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    if (c->is_virtual) {
+        for (int p = 0; p < c->nranks; ++p) {
+            P.bufs[p] = reinterpret_cast<char*>(sends[p]);
+            P.recv[p] = mode == 2 ? nullptr : reinterpret_cast<char*>(recvs[p]);
+            vec = vec && aligned(P.bufs[p]) && (mode == 2 || aligned(P.recv[p]));
+        }
+    } else {
+        char* mine_s = reinterpret_cast<char*>(sends[0]);
+        char* mine_r = mode == 2 ? nullptr : reinterpret_cast<char*>(recvs[0]);
+        // the buffer peers access must be registered (symmetric), at the same offset on every rank
+        char* shared = mode == 1 ? mine_r : mine_s;
+        const size_t ext = mode == 2 ? blk : blk * (size_t)c->nranks;
+        const Registration* reg = find_reg(c, shared, ext);
+        if (!reg) return POLAR_EINVAL;
+        const size_t off = (size_t)(shared - reg->base);
+        for (int p = 0; p < c->nranks; ++p) {
+            char* peer = reg->peer[p] + off;
+            if (mode == 1) {
+                P.recv[p] = peer;
+            } else {
+                P.bufs[p] = peer;
+            }
+            vec = vec && aligned(peer);
+        }
+        if (mode == 0) P.recv[c->rank0] = mine_r;
+        if (mode == 1) P.bufs[c->rank0] = mine_s;
+        vec = vec && aligned(mine_s) && (mode == 2 || aligned(mine_r));
+    }
+    P.vec = vec;
+    return launch_kernel(c, fn, P, grid, stream);
+}
+
 }  // namespace
 
 extern "C" {
@@ -671,6 +749,46 @@ polar_status polar_allreduce_forced(polar_comm_t comm, void* const* bufs, size_t
                                     polar_op op, const polar_decision* forced, void* stream) {
     if (!comm || !forced) return POLAR_EINVAL;
     return do_allreduce(comm, bufs, count, dtype, op, forced, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_reduce_scatter(polar_comm_t comm, const void* sendbuf, void* recvbuf, size_t recvcount,
+                                  polar_dtype dtype, polar_op op, void* stream) {
+    if (!comm || comm->nlocal != 1) return POLAR_EINVAL;
+    void* s[1] = {const_cast<void*>(sendbuf)};
+    void* r[1] = {recvbuf};
+    return do_direct(comm, 0, s, r, recvcount, dtype, op, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_reduce_scatter_v(polar_comm_t comm, void* const* sendbufs, void* const* recvbufs, size_t recvcount,
+                                    polar_dtype dtype, polar_op op, void* stream) {
+    if (!comm) return POLAR_EINVAL;
+    return do_direct(comm, 0, sendbufs, recvbufs, recvcount, dtype, op, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_all_gather(polar_comm_t comm, const void* sendbuf, void* recvbuf, size_t sendcount,
+                              polar_dtype dtype, void* stream) {
+    if (!comm || comm->nlocal != 1) return POLAR_EINVAL;
+    void* s[1] = {const_cast<void*>(sendbuf)};
+    void* r[1] = {recvbuf};
+    return do_direct(comm, 1, s, r, sendcount, dtype, POLAR_SUM, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_all_gather_v(polar_comm_t comm, void* const* sendbufs, void* const* recvbufs, size_t sendcount,
+                                polar_dtype dtype, void* stream) {
+    if (!comm) return POLAR_EINVAL;
+    return do_direct(comm, 1, sendbufs, recvbufs, sendcount, dtype, POLAR_SUM, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_broadcast(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, int root, void* stream) {
+    if (!comm || comm->nlocal != 1) return POLAR_EINVAL;
+    void* b[1] = {buf};
+    return do_direct(comm, 2, b, nullptr, count, dtype, POLAR_SUM, root, reinterpret_cast<cudaStream_t>(stream));
+}
+
+polar_status polar_broadcast_v(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype, int root,
+                               void* stream) {
+    if (!comm) return POLAR_EINVAL;
+    return do_direct(comm, 2, bufs, nullptr, count, dtype, POLAR_SUM, root, reinterpret_cast<cudaStream_t>(stream));
 }
 
 polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, void* const* dev_bufs, size_t count,

@@ -47,6 +47,9 @@ struct Params {
                                 // signal and LL stores (POLAR_JITTER_NS; 0 = off)
     TelEntry* tel;              // profiler telemetry ring (host-mapped), or null
     unsigned long long seq;     // this launch's sequence number in the ring
+    // direct collectives (ReduceScatter / AllGather / Broadcast)
+    char* recv[kMaxRanks];      // rank p's receive buffer (RS / AG), peer-mapped
+    int root;                   // Broadcast root
 };
 
 

@@ -11,6 +11,21 @@ const void* kernel_i64(int op, int algo, int proto);
 const void* kernel_f32(int op, int algo, int proto);
 const void* kernel_bf16(int op, int algo, int proto);
 const void* init_barrier_kernel_ptr();
+// direct collectives: mode 0 = ReduceScatter (op used), 1 = AllGather, 2 = Broadcast
+const void* direct_kernel_i32(int mode, int op);
+const void* direct_kernel_i64(int mode, int op);
+const void* direct_kernel_f32(int mode, int op);
+const void* direct_kernel_bf16(int mode, int op);
+
+inline const void* direct_kernel_for(int dtype, int mode, int op) {
+    switch (dtype) {
+        case POLAR_INT32: return direct_kernel_i32(mode, op);
+        case POLAR_INT64: return direct_kernel_i64(mode, op);
+        case POLAR_FLOAT32: return direct_kernel_f32(mode, op);
+        case POLAR_BFLOAT16: return direct_kernel_bf16(mode, op);
+    }
+    return nullptr;
+}
 
 inline const void* kernel_for(int dtype, int op, int algo, int proto) {
     switch (dtype) {

@@ -29,4 +29,18 @@ const void* kernel_bf16(int op, int algo, int proto) {
     return nullptr;
 }
 
+const void* direct_kernel_bf16(int mode, int op) {
+    using namespace dev;
+    switch (mode) {
+        case MODE_RS:
+            if (op == POLAR_SUM) return reinterpret_cast<const void*>(&direct_kernel<POLAR_BFLOAT16, POLAR_SUM, MODE_RS>);
+            if (op == POLAR_MAX) return reinterpret_cast<const void*>(&direct_kernel<POLAR_BFLOAT16, POLAR_MAX, MODE_RS>);
+            if (op == POLAR_MIN) return reinterpret_cast<const void*>(&direct_kernel<POLAR_BFLOAT16, POLAR_MIN, MODE_RS>);
+            return nullptr;
+        case MODE_AG: return reinterpret_cast<const void*>(&direct_kernel<POLAR_BFLOAT16, POLAR_SUM, MODE_AG>);
+        case MODE_BC: return reinterpret_cast<const void*>(&direct_kernel<POLAR_BFLOAT16, POLAR_SUM, MODE_BC>);
+    }
+    return nullptr;
+}
+
 }  // namespace polar

@@ -836,5 +836,64 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
     }
 }
 
+
+// ============================================================ direct collectives
+// ReduceScatter / AllGather / Broadcast through the same hook (SURVEY.md §8(f)
+// f4; oracle/collectives.py): one all-to-all step on peer-mapped symmetric
+// buffers between the two-shot's entry and exit barriers.  P.count = elements
+// per block (RS: recvcount, AG: sendcount, BC: count).
+//   RS: owner r pulls block r from every rank's send buffer, reduces in rank
+//       order, stores its receive buffer            (ingress (n-1)/n of the input)
+//   AG: rank r pushes its block into block r of every rank's receive buffer
+//   BC: every rank pulls root's buffer                (root only synchronises)
+enum { MODE_RS = 0, MODE_AG = 1, MODE_BC = 2 };
+
+template <int DT, int OP, int MODE>
+__global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int ES = DType<DT>::ES;
+    const Who w = who(P);
+    const int n = w.n, tid = w.tid;
+    ChanState* st = chan_state(P, w.r, w.c);
+    const uint64_t e = st->epoch + 1;
+    if (tid < n) jitter(P), st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
+    bool ok = true;
+    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
+    if (!__syncthreads_and(ok)) return;
+    const unsigned long long NP = npacks<ES>(P);
+    const size_t blk_bytes = (size_t)P.count * ES;
+    unsigned long long a, b;
+    split_range(0, NP, P.nch, w.c, a, b);
+    if constexpr (MODE == MODE_RS) {
+        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+            Acc<DT> acc;
+            acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0] + (size_t)w.r * blk_bytes, i));
+            for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p] + (size_t)w.r * blk_bytes, i));
+            store_pack<ES>(P, P.recv[w.r], i, acc_fin<DT>(acc));
+        }
+    } else if constexpr (MODE == MODE_AG) {
+        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+            const uint4 v = load_pack<ES>(P, P.bufs[w.r], i);
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < n) store_pack<ES>(P, P.recv[p] + (size_t)w.r * blk_bytes, i, v);
+        }
+    } else {
+        if (w.r != P.root)
+            for (unsigned long long i = a + tid; i < b; i += blockDim.x)
+                store_pack<ES>(P, P.bufs[w.r], i, load_pack<ES>(P, P.bufs[P.root], i));
+    }
+    __syncthreads();
+    if (tid < n) {
+        fence_acq_rel(P.sys);
+        jitter(P), st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
+    }
+    ok = true;
+    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
+    if (!__syncthreads_and(ok)) return;
+    epoch_publish(P, w, e);
+}
+
 }  // namespace dev
 }  // namespace polar

@@ -30,6 +30,10 @@ const polar_policy_row kDefaultRows[] = {
     {POLAR_COLL_ALLREDUCE, 0, 64 * KiB, POLAR_ALGO_ONESHOT, POLAR_PROTO_LL, 4, 0},
     {POLAR_COLL_ALLREDUCE, 0, 1 * MiB, POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE, 8, 0},
     {POLAR_COLL_ALLREDUCE, 0, ~uint64_t(0), POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE, 32, 0},
+    // other collectives (f4): one direct all-to-all step
+    {POLAR_COLL_ALLGATHER, 0, ~uint64_t(0), POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE, 32, 0},
+    {POLAR_COLL_BROADCAST, 0, ~uint64_t(0), POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE, 32, 0},
+    {POLAR_COLL_REDUCESCATTER, 0, ~uint64_t(0), POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE, 32, 0},
 };
 constexpr uint32_t kNumDefault = sizeof(kDefaultRows) / sizeof(kDefaultRows[0]);
 

@@ -116,6 +116,12 @@ _sigs = {
     "polar_allreduce_v": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_allreduce_forced": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, C.POINTER(Decision), _P]),
     "polar_allreduce_host": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_reduce_scatter": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_reduce_scatter_v": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_all_gather": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_int, _P]),
+    "polar_all_gather_v": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.c_size_t, C.c_int, _P]),
+    "polar_broadcast": (C.c_int, [_P, _P, C.c_size_t, C.c_int, C.c_int, _P]),
+    "polar_broadcast_v": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_comm_last_decision": (C.c_int, [_P, C.POINTER(Decision)]),
     "polar_comm_launches": (C.c_uint64, [_P]),
     "polar_comm_launch_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
@@ -172,12 +178,12 @@ def decide(nranks: int, nbytes: int, coll: int = COLL_ALLREDUCE) -> Decision:
     return d
 
 
-def decide_batch(ctxs):
-    """ctxs: list of (nranks, nbytes) -> list of (algo, proto, nch, generation)."""
+def decide_batch(ctxs, coll: int = COLL_ALLREDUCE):
+    """ctxs: list of (nranks, nbytes) -> list of (algo, proto, nch, generation, flags)."""
     n = len(ctxs)
     a = (Ctx * max(1, n))()
     for i, (nr, b) in enumerate(ctxs):
-        a[i] = Ctx(COLL_ALLREDUCE, nr, b)
+        a[i] = Ctx(coll, nr, b)
     out = (Decision * max(1, n))()
     _check(lib.polar_decide_batch(a, out, n), "polar_decide_batch")
     return [(d.algo, d.proto, d.nchannels, d.generation, d.flags) for d in out[:n]]
@@ -350,6 +356,32 @@ class Comm:
                      PROTO_CODES[proto] if isinstance(proto, str) else proto, nch, 0)
         _check(lib.polar_allreduce_forced(self.h, arr, n, dt, OP_CODES[op], C.byref(d), _stream_ptr(stream)),
                "polar_allreduce_forced")
+
+    def _ptrs(self, tensors):
+        if not isinstance(tensors, (list, tuple)):
+            tensors = [tensors]
+        if len(tensors) != self.nlocal:
+            raise PolarError(EINVAL, f"need {self.nlocal} buffers, got {len(tensors)}")
+        return (C.c_void_p * self.nlocal)(*[t.data_ptr() for t in tensors]), tensors[0]
+
+    def reduce_scatter(self, sends, recvs, op="sum", stream=None):
+        """recv_r = block r of the rank-ordered reduction of the sends (numel(send) = n * numel(recv))."""
+        s, s0 = self._ptrs(sends)
+        r, r0 = self._ptrs(recvs)
+        _check(lib.polar_reduce_scatter_v(self.h, s, r, r0.numel(), _torch_dtype_code(r0), OP_CODES[op],
+                                          _stream_ptr(stream)), "polar_reduce_scatter_v")
+
+    def all_gather(self, sends, recvs, stream=None):
+        """recv = concatenation of every rank's send (numel(recv) = n * numel(send))."""
+        s, s0 = self._ptrs(sends)
+        r, _ = self._ptrs(recvs)
+        _check(lib.polar_all_gather_v(self.h, s, r, s0.numel(), _torch_dtype_code(s0), _stream_ptr(stream)),
+               "polar_all_gather_v")
+
+    def broadcast(self, bufs, root=0, stream=None):
+        b, b0 = self._ptrs(bufs)
+        _check(lib.polar_broadcast_v(self.h, b, b0.numel(), _torch_dtype_code(b0), int(root), _stream_ptr(stream)),
+               "polar_broadcast_v")
 
     def allreduce_host(self, host_tensors, dev_tensors, op="sum", stream=None):
         harr, n, dt = self._bufs(host_tensors)

@@ -84,6 +84,40 @@ def main():
     comm.allreduce_forced(view, "twoshot", "simple", 4)
     torch.cuda.synchronize()
     check("twoshot/simple/registered-view", view, xs, "f32", "sum", True)
+    # other collectives (f4) on registered symmetric buffers
+    from oracle import collectives as OC
+    rc = 10_007
+    xs_rs = synth.gen_ranks("f32", ws * rc, ws, cfg=33, dist="unif")
+    (sym,) = comm.mem_alloc_tensors(ws * rc, torch.float32)
+    sym.copy_(torch.from_numpy(xs_rs[rank]))
+    rs_out = torch.empty(rc, device="cuda")
+    L.lib.polar_reduce_scatter(comm.h, L.C.c_void_p(sym.data_ptr()), L.C.c_void_p(rs_out.data_ptr()), rc, L.FLOAT32,
+                               L.SUM, L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    comm.check()
+    got = rs_out.cpu().numpy()
+    exp = OC.reduce_scatter(xs_rs, "f32", "sum")[rank]
+    results.append({"tag": "rs/registered", "rank": rank, "ok": bool(np.array_equal(got.view(np.uint32), exp.view(np.uint32))),
+                    "identical": True})
+    xs_ag = synth.gen_ranks("i32", rc, ws, cfg=34, dist="full")
+    src = torch.from_numpy(xs_ag[rank]).cuda()
+    sym_i = sym.view(torch.int32)
+    st = L.lib.polar_all_gather(comm.h, L.C.c_void_p(src.data_ptr()), L.C.c_void_p(sym_i.data_ptr()), rc, L.INT32,
+                                L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    results.append({"tag": "ag/registered", "rank": rank, "ok": st == 0 and bool(np.array_equal(
+        sym_i.cpu().numpy(), OC.all_gather(xs_ag))), "identical": True})
+    bc = sym[:rc]
+    bc.copy_(torch.from_numpy(xs_rs[rank][:rc]))
+    st = L.lib.polar_broadcast(comm.h, L.C.c_void_p(bc.data_ptr()), rc, L.FLOAT32, ws - 1,
+                               L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    results.append({"tag": "bc/registered", "rank": rank, "ok": st == 0 and bool(np.array_equal(
+        bc.cpu().numpy(), xs_rs[ws - 1][:rc])), "identical": True})
+    plain = torch.ones(rc, device="cuda")
+    st = L.lib.polar_broadcast(comm.h, L.C.c_void_p(plain.data_ptr()), rc, L.FLOAT32, 0,
+                               L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    results.append({"tag": "bc/unregistered-einval", "rank": rank, "ok": st == L.EINVAL, "identical": True})
     # policy-selected on a plain torch tensor (unregistered: bounce path if two-shot)
     t = to_device(xs[rank], "f32")
     comm.allreduce(t)

@@ -71,6 +71,17 @@ def test_default_table_matches_oracle():
     _compare([])
 
 
+def test_other_collectives_decisions_match_oracle():
+    """f4: the same hook decides ReduceScatter / AllGather / Broadcast (ctx.coll)."""
+    rows = [(OP.COLL_ALLGATHER, 0, 1 << 20, OP.ONESHOT, OP.SIMPLE, 4),
+            (OP.COLL_REDUCESCATTER, 8, 1 << 24, OP.UNSET, OP.UNSET, 7), (0, 0, 100, OP.RING, OP.LL, 2)]
+    L.set_policy(rows)
+    for coll in (OP.COLL_ALLGATHER, OP.COLL_BROADCAST, OP.COLL_REDUCESCATTER, OP.COLL_ALLREDUCE):
+        ctxs = [(n, b) for n in (1, 2, 8) for b in sorted(_rows_thresholds(rows))[:300]]
+        for (n, b), g in zip(ctxs, L.decide_batch(ctxs, coll=coll)):
+            assert g[:3] == OP.decide(rows, coll, n, b), (coll, n, b)
+
+
 def test_listing1_matches_oracle():
     rows, cases, _ = rows_and_cases("listing1_size_aware.txt")
     L.set_policy(rows)
@@ -141,7 +152,7 @@ def test_decide_argument_errors():
         L.decide(9, 10)
     assert e.value.name == "einval"
     with pytest.raises(L.PolarError) as e:
-        L.decide(8, 10, coll=L.COLL_ALLGATHER)
+        L.decide(8, 10, coll=7)
     assert e.value.name == "eunsupported"
 
 

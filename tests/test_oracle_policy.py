@@ -61,7 +61,8 @@ def test_default_table_is_total_and_clamped():
             assert a in (P.TREE, P.RING, P.ONESHOT, P.TWOSHOT)
             assert p in (P.LL, P.SIMPLE)
             assert 1 <= c <= P.MAXCH
-    assert P.decide([], P.COLL_ALLGATHER, 8, 1024) is None
+    assert P.decide([], 7, 8, 1024) is None               # no default row for an unknown collective
+    assert P.decide([], P.COLL_ALLGATHER, 8, 1024) == (P.ONESHOT, P.SIMPLE, 32)
 
 
 def test_first_match_and_nranks_filter():
