@@ -436,3 +436,19 @@ class Comm:
 
 def version() -> str:
     return lib.polar_version().decode()
+
+
+def _load_env_policy():
+    """POLAR_POLICY=path.json installs that policy table at import (SURVEY.md §5
+    "Config / flags"); a rejected table raises (the library keeps noop)."""
+    path = os.environ.get("POLAR_POLICY", "")
+    if not path:
+        return
+    import json
+    with open(path) as f:
+        d = json.load(f)
+    rows = d["rows"] if isinstance(d, dict) else d
+    set_policy([tuple(int(x) for x in r) for r in rows])
+
+
+_load_env_policy()
