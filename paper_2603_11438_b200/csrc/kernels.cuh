@@ -865,24 +865,51 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) 
     const size_t blk_bytes = (size_t)P.count * ES;
     unsigned long long a, b;
     split_range(0, NP, P.nch, w.c, a, b);
+    const unsigned long long stride = (unsigned long long)blockDim.x;
     if constexpr (MODE == MODE_RS) {
-        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
+        // every rank's pack issued before the reduction (n loads in flight per thread)
+        for (unsigned long long i = a + tid; i < b; i += stride) {
+            uint4 v[kMaxRanks];
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < n) v[p] = load_pack<ES>(P, P.bufs[p] + (size_t)w.r * blk_bytes, i);
             Acc<DT> acc;
-            acc_init<DT>(acc, load_pack<ES>(P, P.bufs[0] + (size_t)w.r * blk_bytes, i));
-            for (int p = 1; p < n; ++p) acc_add<DT, OP>(acc, load_pack<ES>(P, P.bufs[p] + (size_t)w.r * blk_bytes, i));
+            acc_init<DT>(acc, v[0]);
+#pragma unroll
+            for (int p = 1; p < kMaxRanks; ++p)
+                if (p < n) acc_add<DT, OP>(acc, v[p]);
             store_pack<ES>(P, P.recv[w.r], i, acc_fin<DT>(acc));
         }
     } else if constexpr (MODE == MODE_AG) {
-        for (unsigned long long i = a + tid; i < b; i += blockDim.x) {
-            const uint4 v = load_pack<ES>(P, P.bufs[w.r], i);
+        constexpr int U = 1;   // (U = 4 measured slower: 454 vs 507 GB/s busBW at 256 MiB)
+        for (unsigned long long i0 = a + tid; i0 < b; i0 += U * stride) {
+            uint4 v[U];
 #pragma unroll
-            for (int p = 0; p < kMaxRanks; ++p)
-                if (p < n) store_pack<ES>(P, P.recv[p] + (size_t)w.r * blk_bytes, i, v);
+            for (int u = 0; u < U; ++u)
+                if (i0 + u * stride < b) v[u] = load_pack<ES>(P, P.bufs[w.r], i0 + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + u * stride < b) {
+#pragma unroll
+                    for (int p = 0; p < kMaxRanks; ++p)
+                        if (p < n) store_pack<ES>(P, P.recv[p] + (size_t)w.r * blk_bytes, i0 + u * stride, v[u]);
+                }
         }
     } else {
+        // Broadcast: every non-root rank pulls the root's slice, 8 packs per thread
+        // in flight.  (Staggering the ranks' pull order was measured slower: the
+        // concurrent pulls of the same root lines are served from L2.)
+        constexpr int U = 8;
         if (w.r != P.root)
-            for (unsigned long long i = a + tid; i < b; i += blockDim.x)
-                store_pack<ES>(P, P.bufs[w.r], i, load_pack<ES>(P, P.bufs[P.root], i));
+            for (unsigned long long i0 = a + tid; i0 < b; i0 += U * stride) {
+                uint4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i0 + u * stride < b) v[u] = load_pack<ES>(P, P.bufs[P.root], i0 + u * stride);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i0 + u * stride < b) store_pack<ES>(P, P.bufs[w.r], i0 + u * stride, v[u]);
+            }
     }
     __syncthreads();
     if (tid < n) {

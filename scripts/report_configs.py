@@ -182,6 +182,29 @@ def c3():
         torch.cuda.empty_cache()
 
 
+def f4():
+    """ReduceScatter / AllGather / Broadcast, 8 virtual ranks, f32.
+    busBW (nccl-tests): RS, AG: S*(n-1)/n / t with S the full buffer; BC: S / t."""
+    n = 8
+    comm = L.Comm.virtual(n, 0)
+    for total in [(64 << 10) << (2 * k) for k in range(0, 7)]:      # 64 KiB .. 256 MiB
+        blk = total // n // 4
+        sends = [torch.randn(n * blk, device="cuda") for _ in range(n)]
+        recvs = [torch.empty(blk, device="cuda") for _ in range(n)]
+        agsend = [torch.randn(blk, device="cuda") for _ in range(n)]
+        agrecv = [torch.empty(n * blk, device="cuda") for _ in range(n)]
+        rec = {"config": "F4", "n": n, "dtype": "f32", "bytes": total}
+        for name, fn, bb in (("reduce_scatter", lambda: comm.reduce_scatter(sends, recvs), total * (n - 1) / n),
+                             ("all_gather", lambda: comm.all_gather(agsend, agrecv), total * (n - 1) / n),
+                             ("broadcast", lambda: comm.broadcast(agrecv, root=3), total)):
+            it, _ = iters_for(fn, 0.05)
+            t = ev_time(fn, it)
+            rec[name] = {"busbw_gbs": round(bb / t / 1e9, 1), "us": round(t * 1e6, 1)}
+        emit(rec)
+        del sends, recvs, agsend, agrecv
+    comm.destroy()
+
+
 def c5():
     ctxs = [(nr, 1 << k) for k in range(3, 31) for nr in (2, 4, 8)]
     s = L.bench_decide(ctxs, nwarm=10_000, ncalls=400_000)
@@ -198,11 +221,11 @@ def c5():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,2,3,5")
+    ap.add_argument("--configs", default="1,2,3,5,f4")
     a = ap.parse_args()
     t0 = time.time()
     for c in a.configs.split(","):
-        {"1": c1, "2": c2, "3": c3, "5": c5}[c.strip()]()
+        {"1": c1, "2": c2, "3": c3, "5": c5, "f4": f4}[c.strip()]()
     emit({"elapsed_s": round(time.time() - t0, 1), "cpu_cores": len(os.sched_getaffinity(0))})
 
 
