@@ -205,6 +205,44 @@ def f4():
     comm.destroy()
 
 
+def e12():
+    """Stability (PAPER.md L588-595 method): 20 independent runs at 128 MiB, 8 ranks,
+    each the mean of 20 timed calls after warm-up; mean +- sd and CV of busBW, for
+    the policy-selected AllReduce and for AllGather (the paper's collective)."""
+    n, size = 8, 128 << 20
+    comm = L.Comm.virtual(n, 0)
+    bufs = [torch.empty(size // 4, device="cuda").uniform_(-1, 1) for _ in range(n)]
+    ag_s = [torch.randn(size // 4 // n, device="cuda") for _ in range(n)]
+    ag_r = [torch.empty(size // 4, device="cuda") for _ in range(n)]
+    for name, fn, bb in (("allreduce", lambda: comm.allreduce(bufs), size * 2 * (n - 1) / n),
+                         ("all_gather", lambda: comm.all_gather(ag_s, ag_r), size * (n - 1) / n)):
+        runs = [bb / ev_time(fn, 20, warm=5) / 1e9 for _ in range(20)]
+        m, sd = float(np.mean(runs)), float(np.std(runs, ddof=1))
+        emit({"config": "E12", "op": name, "n": n, "bytes": size, "runs": 20,
+              "busbw_mean_gbs": round(m, 2), "busbw_sd_gbs": round(sd, 2), "cv_pct": round(100 * sd / m, 3)})
+    comm.destroy()
+
+
+def table2():
+    """PAPER.md Table 2 sizes on this box (8 ranks, f32 sum): the policy's choice vs
+    ring (the paper's winner in 4-128 MiB) at 256 MiB, 1 GiB and 8 GiB."""
+    n = 8
+    comm = L.Comm.virtual(n, 0)
+    for size in (256 << 20, 1 << 30, 8 << 30):
+        bufs = [torch.empty(size // 4, device="cuda").uniform_(-1, 1) for _ in range(n)]
+        rec = {"config": "T2", "n": n, "dtype": "f32", "bytes": size}
+        t = ev_time(lambda: comm.allreduce(bufs), 3, warm=1)
+        d = comm.last_decision()
+        rec["policy"] = {"decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
+                         "busbw_gbs": round(busbw(size, n, t), 1)}
+        t = ev_time(lambda: comm.allreduce_forced(bufs, "ring", "simple", 32), 2, warm=1)
+        rec["ring_simple"] = {"busbw_gbs": round(busbw(size, n, t), 1)}
+        emit(rec)
+        del bufs
+        torch.cuda.empty_cache()
+    comm.destroy()
+
+
 def c5():
     ctxs = [(nr, 1 << k) for k in range(3, 31) for nr in (2, 4, 8)]
     s = L.bench_decide(ctxs, nwarm=10_000, ncalls=400_000)
@@ -221,11 +259,11 @@ def c5():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,2,3,5,f4")
+    ap.add_argument("--configs", default="1,2,3,5,f4,e12,t2")
     a = ap.parse_args()
     t0 = time.time()
     for c in a.configs.split(","):
-        {"1": c1, "2": c2, "3": c3, "5": c5, "f4": f4}[c.strip()]()
+        {"1": c1, "2": c2, "3": c3, "5": c5, "f4": f4, "e12": e12, "t2": table2}[c.strip()]()
     emit({"elapsed_s": round(time.time() - t0, 1), "cpu_cores": len(os.sched_getaffinity(0))})
 
 
