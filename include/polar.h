@@ -200,7 +200,9 @@ polar_status polar_bootstrap_check(int nranks, int rank, polar_allgather_fn ag, 
  * protocols; peers are local HBM instead of NVLink. */
 polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device);
 
-polar_status polar_comm_destroy(polar_comm_t comm);   /* collective for real comms */
+/* Collective for real comms: synchronises the device, host-barriers through the
+ * all-gather (no peer still touches this rank's memory), then unmaps and frees. */
+polar_status polar_comm_destroy(polar_comm_t comm);
 
 /* nranks, this process's first rank, and how many ranks this process hosts
  * (1 for a real comm, nranks for a virtual one).  Any out pointer may be NULL. */
@@ -210,6 +212,7 @@ polar_status polar_comm_info(polar_comm_t comm, int* nranks, int* rank, int* nlo
  * peer-mapped on every rank, so AllReduce on it is zero-copy.  ptrs receives
  * nlocal device pointers.  Freed by polar_mem_free (collective) or destroy. */
 polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs);
+/* Collective for real comms (barrier, unmap the peers' copies, barrier, free). */
 polar_status polar_mem_free(polar_comm_t comm, void* ptr);
 
 /* Register caller-owned device memory [buf, buf+bytes) for zero-copy use

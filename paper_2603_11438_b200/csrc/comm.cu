@@ -271,10 +271,21 @@ const Registration* find_reg(const polar_comm_s* c, const char* p, size_t bytes)
     return nullptr;
 }
 
-void destroy_comm(polar_comm_s* c) {
+// Host barrier over the bootstrap all-gather (real comms): every rank's device
+// work has completed before anyone unmaps or frees memory a peer may still be
+// touching (a final credit or exit flag posted into my scratch after my kernel
+// returned, for example).
+polar_status host_barrier(polar_comm_s* c) {
+    if (c->is_virtual || c->nranks == 1 || !c->ag) return POLAR_OK;
+    uint64_t mine = 0x62617272ull, all[kMaxRanks];
+    return c->ag(&mine, all, sizeof(uint64_t), c->user) == 0 ? POLAR_OK : POLAR_ESTATE;
+}
+
+void destroy_comm(polar_comm_s* c, bool collective) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    if (collective) (void)host_barrier(c);
     for (char* m : c->ipc_mapped) cudaIpcCloseMemHandle(m);
     for (auto& r : c->regs)
         if (r.owned) cudaFree(r.base);
@@ -600,7 +611,7 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     if (st == POLAR_OK) st = bootstrap_check(nranks, rank, c->L, ag, user);
     if (st == POLAR_OK) st = exchange_and_map(c, c->scratch_own[0], c->scratch);
     if (st == POLAR_OK) st = init_barrier(c);
-    if (st != POLAR_OK) { destroy_comm(c); return st; }
+    if (st != POLAR_OK) { destroy_comm(c, false); return st; }
     *out = c;
     return POLAR_OK;
 }
@@ -652,14 +663,14 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
     }
     if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
     if (st == POLAR_OK) st = init_barrier(c);
-    if (st != POLAR_OK) { destroy_comm(c); return st; }
+    if (st != POLAR_OK) { destroy_comm(c, false); return st; }
     *out = c;
     return POLAR_OK;
 }
 
 polar_status polar_comm_destroy(polar_comm_t comm) {
     if (!comm) return POLAR_EINVAL;
-    destroy_comm(comm);
+    destroy_comm(comm, true);
     return POLAR_OK;
 }
 
@@ -708,10 +719,29 @@ polar_status polar_mem_free(polar_comm_t comm, void* ptr) {
         }
     for (size_t i = 0; i < comm->regs.size(); ++i)
         if (comm->regs[i].base == ptr && comm->regs[i].owned) {
-            // peers' mappings of this buffer stay open until destroy (IPC handles are per allocation)
+            // collective: everyone is done with every copy, everyone unmaps the
+            // peers' copies (each owned buffer is its own allocation, mapped at
+            // offset 0), everyone has unmapped, then each rank frees its own
+            polar_status st = host_barrier(comm);
+            const Registration r = comm->regs[i];
+            for (int p = 0; p < comm->nranks; ++p) {
+                if (p == comm->rank0) continue;
+                for (size_t k = 0; k < comm->opened.size(); ++k)
+                    if (comm->opened[k].peer == p && comm->opened[k].base == r.peer[p]) {
+                        cudaIpcCloseMemHandle(r.peer[p]);
+                        comm->opened.erase(comm->opened.begin() + (long)k);
+                        for (size_t m = 0; m < comm->ipc_mapped.size(); ++m)
+                            if (comm->ipc_mapped[m] == r.peer[p]) {
+                                comm->ipc_mapped.erase(comm->ipc_mapped.begin() + (long)m);
+                                break;
+                            }
+                        break;
+                    }
+            }
+            if (st == POLAR_OK) st = host_barrier(comm);
             cudaFree(ptr);
             comm->regs.erase(comm->regs.begin() + (long)i);
-            return POLAR_OK;
+            return st;
         }
     return POLAR_EINVAL;
 }

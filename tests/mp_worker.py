@@ -118,6 +118,16 @@ def main():
     st = L.lib.polar_broadcast(comm.h, L.C.c_void_p(plain.data_ptr()), rc, L.FLOAT32, 0,
                                L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
     results.append({"tag": "bc/unregistered-einval", "rank": rank, "ok": st == L.EINVAL, "identical": True})
+    # collective free of a symmetric buffer, then a fresh allocation still works
+    sym_ptr = sym.data_ptr()
+    del sym, sym_i, bc
+    comm.mem_free(sym_ptr)
+    (again,) = comm.mem_alloc_tensors(4096, torch.float32)
+    again.fill_(float(rank + 1))
+    comm.allreduce_forced(again, "twoshot", "simple", 2)
+    torch.cuda.synchronize()
+    results.append({"tag": "mem_free+realloc", "rank": rank, "ok": bool((again == ws * (ws + 1) / 2).all()),
+                    "identical": True})
     # policy-selected on a plain torch tensor (unregistered: bounce path if two-shot)
     t = to_device(xs[rank], "f32")
     comm.allreduce(t)
