@@ -124,6 +124,21 @@ namespace {
 
 inline polar_status cuerr(cudaError_t e) { return e == cudaSuccess ? POLAR_OK : POLAR_ECUDA; }
 
+// Make `dev` current for the scope and restore the caller's device on exit:
+// no C-ABI entry point changes the calling thread's current device.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = (prev == dev) || cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 #define CU_TRY(x)                                   \
     do {                                            \
         cudaError_t _e = (x);                       \
@@ -283,7 +298,7 @@ polar_status host_barrier(polar_comm_s* c) {
 
 void destroy_comm(polar_comm_s* c, bool collective) {
     if (!c) return;
-    cudaSetDevice(c->device);
+    DeviceGuard dg(c->device);
     cudaDeviceSynchronize();
     if (collective) (void)host_barrier(c);
     for (char* m : c->ipc_mapped) cudaIpcCloseMemHandle(m);
@@ -444,7 +459,8 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     }
     c->last_nch = d.nchannels;        // what is launched
     if (count == 0 || c->nranks == 1) return POLAR_OK;
-    if (cudaSetDevice(c->device) != cudaSuccess) return POLAR_ECUDA;
+    DeviceGuard dg(c->device);
+    if (!dg.ok) return POLAR_ECUDA;
 
     dev::Params P;
     fill_params(c, P);
@@ -537,7 +553,8 @@ polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* cons
     }
     c->last_nch = d.nchannels;
     if (count == 0) return POLAR_OK;
-    if (cudaSetDevice(c->device) != cudaSuccess) return POLAR_ECUDA;
+    DeviceGuard dg(c->device);
+    if (!dg.ok) return POLAR_ECUDA;
     const size_t blk = count * (size_t)es;
     if (c->nranks == 1) {   // identity collectives: copy send -> recv where they differ
         if (mode != 2 && sends[0] != recvs[0])
@@ -603,7 +620,8 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     c->ag = ag;
     c->user = user;
     c->L = make_layout(true);
-    polar_status st = cuerr(cudaSetDevice(cuda_device));
+    DeviceGuard dg(cuda_device);
+    polar_status st = dg.ok ? POLAR_OK : POLAR_ECUDA;
     if (st == POLAR_OK) st = alloc_common(c);
     if (st == POLAR_OK) st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[0]), c->L.total));
     if (st == POLAR_OK) st = cuerr(cudaMemset(c->scratch_own[0], 0, c->L.total));
@@ -637,7 +655,8 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
         c->coop = !(ev && ev[0] == '0');
     }
     c->L = make_layout(false);
-    polar_status st = cuerr(cudaSetDevice(cuda_device));
+    DeviceGuard dg(cuda_device);
+    polar_status st = dg.ok ? POLAR_OK : POLAR_ECUDA;
     if (st == POLAR_OK) st = alloc_common(c);
     for (int p = 0; p < nranks && st == POLAR_OK; ++p) {
         st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[p]), c->L.total));
@@ -685,7 +704,8 @@ polar_status polar_comm_info(polar_comm_t comm, int* nranks, int* rank, int* nlo
 polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs) {
     if (!comm || !ptrs || bytes == 0) return POLAR_EINVAL;
     std::lock_guard<std::mutex> lk(comm->mu);
-    CU_TRY(cudaSetDevice(comm->device));
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
     if (comm->is_virtual) {
         for (int p = 0; p < comm->nranks; ++p) {
             char* m = nullptr;
@@ -709,7 +729,7 @@ polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs) {
 polar_status polar_mem_free(polar_comm_t comm, void* ptr) {
     if (!comm || !ptr) return POLAR_EINVAL;
     std::lock_guard<std::mutex> lk(comm->mu);
-    cudaSetDevice(comm->device);
+    DeviceGuard dg(comm->device);
     cudaDeviceSynchronize();
     for (size_t i = 0; i < comm->virt_allocs.size(); ++i)
         if (comm->virt_allocs[i] == ptr) {
@@ -750,7 +770,8 @@ polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes) {
     if (!comm || !buf || bytes == 0) return POLAR_EINVAL;
     if (comm->is_virtual) return POLAR_OK;
     std::lock_guard<std::mutex> lk(comm->mu);
-    CU_TRY(cudaSetDevice(comm->device));
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
     Registration r{};
     r.base = reinterpret_cast<char*>(buf);
     r.bytes = bytes;
@@ -827,7 +848,8 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
     const int es = esize_of(dtype);
     if (!es) return POLAR_EINVAL;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    CU_TRY(cudaSetDevice(comm->device));
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
     const size_t bytes = count * (size_t)es;
     for (int l = 0; l < comm->nlocal && count; ++l)
         CU_TRY(cudaMemcpyAsync(dev_bufs[l], host_bufs[l], bytes, cudaMemcpyHostToDevice, s));
