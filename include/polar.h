@@ -37,7 +37,7 @@ typedef enum {
     POLAR_OK = 0,
     POLAR_EINVAL = 1,        /* malformed argument or policy table                   */
     POLAR_ECUDA = 2,         /* a CUDA runtime/driver call failed                     */
-    POLAR_EUNSUPPORTED = 3,  /* well-formed but not built (NVLS, LL128, other colls)  */
+    POLAR_EUNSUPPORTED = 3,  /* well-formed but not built (NVLS; no kernel for a decision) */
     POLAR_ETIMEOUT = 4,      /* a device-side wait for a peer exceeded the timeout    */
     POLAR_EBUSY = 5,         /* concurrent use of a single-threaded object            */
     POLAR_ESTATE = 6,        /* comm unusable (earlier latched error / destroyed)     */
@@ -55,7 +55,7 @@ enum { POLAR_COLL_ALLREDUCE = 0, POLAR_COLL_ALLGATHER = 1, POLAR_COLL_BROADCAST 
        POLAR_COLL_REDUCESCATTER = 3 };
 enum { POLAR_ALGO_TREE = 0, POLAR_ALGO_RING = 1, POLAR_ALGO_NVLS = 2 /* reserved */,
        POLAR_ALGO_ONESHOT = 3, POLAR_ALGO_TWOSHOT = 4 };
-enum { POLAR_PROTO_LL = 0, POLAR_PROTO_LL128 = 1 /* reserved */, POLAR_PROTO_SIMPLE = 2 };
+enum { POLAR_PROTO_LL = 0, POLAR_PROTO_LL128 = 1, POLAR_PROTO_SIMPLE = 2 };
 
 #define POLAR_UNSET 0xFFFFFFFFu   /* algo/proto "defer to default"   */
 #define POLAR_MAXCH 32            /* channel clamp bound (R8) */
@@ -115,7 +115,8 @@ typedef struct polar_comm_s* polar_comm_t;   /* opaque; owned by the library */
  * compare-and-swap on the pointer").  The rows are COPIED.
  * Validation: nrows <= 64; known enums; nranks <= 8; only known flag bits; rows of one
  * (coll, nranks) group strictly ascending in max_bytes -> else POLAR_EINVAL;
- * NVLS or LL128 -> POLAR_EUNSUPPORTED.  On any rejection the active policy and
+ * NVLS -> POLAR_EUNSUPPORTED (LL128 is accepted: every algorithm has an LL128
+ * kernel).  On any rejection the active policy and
  * its generation are unchanged ("the old policy continues").
  * nrows == 0 installs the empty policy (the paper's `noop`, L433).
  * On success the generation increases by exactly 1 and is stored in

@@ -102,7 +102,8 @@ def validate(rows) -> str:
 
     "ok", or "einval" (malformed: too many rows, unknown enum, nranks > 8,
     rows of one (coll, nranks) group not strictly ascending in max_bytes), or
-    "eunsupported" (well-formed but names NVLS or LL128, not built yet).
+    "eunsupported" (well-formed but names NVLS, not built yet).  LL128 is
+    accepted: the protocol exists.
     """
     if len(rows) > MAXROWS:
         return "einval"
@@ -127,6 +128,6 @@ def validate(rows) -> str:
         if key in last and max_bytes <= last[key]:
             return "einval"
         last[key] = max_bytes
-        if algo == NVLS or proto == LL128:
+        if algo == NVLS:
             unsupported = True
     return "eunsupported" if unsupported else "ok"

@@ -67,6 +67,12 @@ Layout make_layout(bool with_bounce) {
     L.tree_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.tree_slot, 4096);
     L.treell_slot = align_up(env_size("POLAR_TREELL_SLOT", 64 << 10), 512);
     L.treell_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.treell_slot, 4096);
+    L.os128_off = off; off = align_up(off + 2 * kMaxRanks * 2 * L.osll_chunk, 4096);
+    L.ts128_off = off; off = align_up(off + 2 * (2 * kMaxRanks * 2 * L.tsll_chunk), 4096);
+    L.ring128_slot = align_up(env_size("POLAR_RING128_SLOT", 128 << 10), 512);
+    L.ring128_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring128_slot, 4096);
+    L.tree128_slot = align_up(env_size("POLAR_TREE128_SLOT", 64 << 10), 512);
+    L.tree128_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.tree128_slot, 4096);
     L.bounce_bytes = with_bounce ? align_up(env_size("POLAR_BOUNCE", 64 << 20), 4096) : 0;
     L.bounce_off = off; off = align_up(off + L.bounce_bytes, 4096);
     L.total = off;
@@ -172,6 +178,9 @@ void fill_params(const polar_comm_s* c, dev::Params& P) {
     P.ringll_off = L.ringll_off; P.ringll_slot = L.ringll_slot;
     P.tree_off = L.tree_off; P.tree_slot = L.tree_slot;
     P.treell_off = L.treell_off; P.treell_slot = L.treell_slot;
+    P.os128_off = L.os128_off; P.ts128_off = L.ts128_off;
+    P.ring128_off = L.ring128_off; P.ring128_slot = L.ring128_slot;
+    P.tree128_off = L.tree128_off; P.tree128_slot = L.tree128_slot;
     P.trace = c->trace;
     P.sys = c->is_virtual ? 0 : 1;
     P.jitter_ns = c->jitter_ns;
@@ -670,7 +679,7 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
         const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
         const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
         const int algos[] = {POLAR_ALGO_TREE, POLAR_ALGO_RING, POLAR_ALGO_ONESHOT, POLAR_ALGO_TWOSHOT};
-        const int protos[] = {POLAR_PROTO_LL, POLAR_PROTO_SIMPLE};
+        const int protos[] = {POLAR_PROTO_LL, POLAR_PROTO_LL128, POLAR_PROTO_SIMPLE};
         for (int dt : dts) for (int op : ops) for (int a : algos) for (int pr : protos) {
             if (st != POLAR_OK) break;
             const void* fn = kernel_for(dt, op, a, pr);

@@ -40,6 +40,9 @@ struct Params {
     unsigned long long os_off, os_chunk, osll_off, osll_chunk, tsll_off, tsll_chunk;
     unsigned long long ring_off, ring_slot, ringll_off, ringll_slot;
     unsigned long long tree_off, tree_slot, treell_off, treell_slot;
+    // LL128 regions (own memory: a stale line of another protocol must never be
+    // read as LL128 and vice versa); staging slots are as large as the LL ones
+    unsigned long long os128_off, ts128_off, ring128_off, ring128_slot, tree128_off, tree128_slot;
     unsigned long long* trace;  // optional per-CTA timestamps (polar_comm_set_trace), else null
     int sys;                    // 1: peers are other GPUs (system-scope ordering); 0: one GPU (gpu scope)
     int tma;                    // two-shot Simple: 1 = TMA bulk-copy staging through shared memory
@@ -116,6 +119,37 @@ __device__ __forceinline__ uint4 ld_ll(const uint4* p) {
                  : "l"(p)
                  : "memory");
     return v;
+}
+
+// LL128 (the protocol the paper's `nvlink_ring_mid_v2` policy
+// selects for 4-32 MiB).  One warp moves a UNIT of 30 packs
+// (480 B payload) as one group of 4 x 128-B lines (512 B on the wire, 93.75 %
+// payload): in line g (lanes 8g..8g+7) lanes 8g..8g+6 carry packs 7g..7g+6 and
+// lane 8g+7 carries 8 B of pack 28 + g/2 (low half for even g, high half for odd
+// g) followed by the u64 flag in the line's last 8 B.  Each lane writes its 16 B
+// with one st.volatile.v4; the warp's store of a 128-B line lands as one unit
+// (the property NCCL's LL128 also relies on), so a reader that sees the flag of
+// a line sees its data.  Readers load whole line groups and retry until all four
+// flags match.  Warp-collective: every lane of the warp must call both.
+constexpr int kLL128Packs = 30;
+constexpr int kLL128UnitBytes = 512;
+
+__device__ __forceinline__ void st_ll128(uint4* group, uint4 v, uint64_t flag) {
+    const int lane = (int)(threadIdx.x & 31), g = lane >> 3, q = lane & 7;
+    const int src = q < 7 ? g * 7 + q : 28 + (g >> 1);
+    uint4 w;
+    w.x = __shfl_sync(0xffffffffu, v.x, src);
+    w.y = __shfl_sync(0xffffffffu, v.y, src);
+    w.z = __shfl_sync(0xffffffffu, v.z, src);
+    w.w = __shfl_sync(0xffffffffu, v.w, src);
+    if (q == 7) {
+        if (g & 1) { w.x = w.z; w.y = w.w; }
+        w.z = (uint32_t)flag;
+        w.w = (uint32_t)(flag >> 32);
+    }
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(group + lane), "r"(w.x), "r"(w.y), "r"(w.z),
+                 "r"(w.w)
+                 : "memory");
 }
 
 // ----------------------------------------------------- TMA bulk copies + mbarrier
@@ -223,6 +257,42 @@ __device__ __forceinline__ bool poll_ll(const Params& P, const uint4* p, uint32_
             if (*(volatile int*)P.err) return false;
         }
     }
+}
+
+// Poll one LL128 line group until all four flags equal `flag`, then hand lane
+// L < 30 its pack L (lanes 30, 31 get padding).  Warp-uniform result; false on
+// timeout (error latched).
+__device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, uint64_t flag, uint4& out) {
+    const int lane = (int)(threadIdx.x & 31), q = lane & 7;
+    const uint32_t flo = (uint32_t)flag, fhi = (uint32_t)(flag >> 32);
+    uint4 w;
+    uint64_t t0 = 0;
+    for (uint32_t it = 0;; ++it) {
+        w = ld_ll(group + lane);
+        const bool mine = q != 7 || (w.z == flo && w.w == fhi);
+        if (__all_sync(0xffffffffu, mine)) break;
+        if ((it & 1023) == 1023) {
+            int bad = 0;
+            if (lane == 0) {
+                const uint64_t now = globaltimer();
+                if (t0 == 0) t0 = now;
+                if (now - t0 > P.timeout_ns) { raise_error(P, POLAR_ETIMEOUT); bad = 1; }
+                else if (*(volatile int*)P.err) bad = 1;
+            }
+            if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+        }
+    }
+    const int s0 = lane < 28 ? (lane / 7) * 8 + lane % 7 : (lane == 28 ? 7 : 23);
+    const int s1 = lane == 29 ? 31 : 15;
+    uint4 a;
+    a.x = __shfl_sync(0xffffffffu, w.x, s0);
+    a.y = __shfl_sync(0xffffffffu, w.y, s0);
+    a.z = __shfl_sync(0xffffffffu, w.z, s0);
+    a.w = __shfl_sync(0xffffffffu, w.w, s0);
+    const uint32_t b0 = __shfl_sync(0xffffffffu, w.x, s1);
+    const uint32_t b1 = __shfl_sync(0xffffffffu, w.y, s1);
+    out = lane < 28 ? a : make_uint4(a.x, a.y, b0, b1);
+    return true;
 }
 
 // ------------------------------------------------------------ scratch access

@@ -7,15 +7,23 @@ namespace polar {
 template <int OP, int ALGO, int PROTO>
 static const void* k() { return reinterpret_cast<const void*>(&dev::allreduce_kernel<POLAR_INT64, OP, ALGO, PROTO>); }
 
+template <int OP, int PROTO>
+static const void* by_algo_p(int algo) {
+    switch (algo) {
+        case POLAR_ALGO_TWOSHOT: return k<OP, POLAR_ALGO_TWOSHOT, PROTO>();
+        case POLAR_ALGO_ONESHOT: return k<OP, POLAR_ALGO_ONESHOT, PROTO>();
+        case POLAR_ALGO_RING: return k<OP, POLAR_ALGO_RING, PROTO>();
+        case POLAR_ALGO_TREE: return k<OP, POLAR_ALGO_TREE, PROTO>();
+    }
+    return nullptr;
+}
+
 template <int OP>
 static const void* by_algo(int algo, int proto) {
-    const bool ll = proto == POLAR_PROTO_LL;
-    if (proto != POLAR_PROTO_LL && proto != POLAR_PROTO_SIMPLE) return nullptr;
-    switch (algo) {
-        case POLAR_ALGO_TWOSHOT: return ll ? k<OP, POLAR_ALGO_TWOSHOT, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE>();
-        case POLAR_ALGO_ONESHOT: return ll ? k<OP, POLAR_ALGO_ONESHOT, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_ONESHOT, POLAR_PROTO_SIMPLE>();
-        case POLAR_ALGO_RING: return ll ? k<OP, POLAR_ALGO_RING, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_RING, POLAR_PROTO_SIMPLE>();
-        case POLAR_ALGO_TREE: return ll ? k<OP, POLAR_ALGO_TREE, POLAR_PROTO_LL>() : k<OP, POLAR_ALGO_TREE, POLAR_PROTO_SIMPLE>();
+    switch (proto) {
+        case POLAR_PROTO_LL: return by_algo_p<OP, POLAR_PROTO_LL>(algo);
+        case POLAR_PROTO_LL128: return by_algo_p<OP, POLAR_PROTO_LL128>(algo);
+        case POLAR_PROTO_SIMPLE: return by_algo_p<OP, POLAR_PROTO_SIMPLE>(algo);
     }
     return nullptr;
 }

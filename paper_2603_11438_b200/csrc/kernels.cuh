@@ -51,20 +51,22 @@ __device__ __forceinline__ void epoch_publish(const Params& P, const Who& w, uin
 // last chunk must not re-slice: a lagging peer channel may still be polling the
 // same-parity slot of two chunks ago).  `per` is the same on every rank and for
 // every chunk of a call: min(slot capacity / nch, ceil(NP / (parts*nch))),
-// rounded to whole 512-B units.
+// rounded to whole UNITs (32 packs = 512 B; 30 packs = one LL128 warp unit, so
+// that channel regions start on a line group).
 struct Geo {
     unsigned long long per;      // packs per channel per part per chunk
     unsigned long long part;     // per * nch: packs per part (owner) per chunk
     unsigned long long chunk;    // part * parts
     unsigned long long nchunks;
 };
+template <unsigned long long UNIT>
 __device__ __forceinline__ Geo make_geo(unsigned long long NP, unsigned long long cap_packs, int nch, int parts) {
     Geo g;
-    unsigned long long cap = (cap_packs / (unsigned long long)nch) / kUnit * kUnit;
+    unsigned long long cap = (cap_packs / (unsigned long long)nch) / UNIT * UNIT;
     unsigned long long need = (NP + (unsigned long long)(parts * nch) - 1) / (unsigned long long)(parts * nch);
-    need = (need + kUnit - 1) / kUnit * kUnit;
+    need = (need + UNIT - 1) / UNIT * UNIT;
     g.per = need < cap ? need : cap;
-    if (g.per < kUnit) g.per = kUnit;
+    if (g.per < UNIT) g.per = UNIT;
     g.part = g.per * (unsigned long long)nch;
     g.chunk = g.part * (unsigned long long)parts;
     g.nchunks = (NP + g.chunk - 1) / g.chunk;
@@ -338,85 +340,160 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     epoch_publish(P, w, e);
 }
 
-// Two-shot LL: push-based.  RS: rank r writes its part of owner j's shard as LL
-// lines into j's RS staging slot r; owner polls, reduces in rank order, writes
-// its own buffer and pushes the result as LL lines into every rank's AG slot;
-// every rank polls the AG slots.  Two NVLink hops, no separate flags.
+// ====================================================================== wires
+// How packs travel through staging slots and FIFOs, per protocol.  A slot is
+// addressed by WIRE INDEX k: Simple = one 16-B pack, LL = one pack as two 16-B LL
+// lines, LL128 = one warp unit of kLL128Packs packs as a 512-B line group.
+// put/get of LL128 are warp-collective (every lane calls them; see for_packs).
+//   Simple: payload only; ordering comes from a separate fence + flag.
+//   LL    : flag-in-data, flag = (u32) sequence number.
+//   LL128 : flag per 128-B line, flag = u64 sequence number.
 
-__device__ __forceinline__ uint4* tsll_rs(const Params& P, int owner, int par, int slot) {
-    return reinterpret_cast<uint4*>(P.scratch[owner] + P.tsll_off +
+template <int PROTO> struct Wire;
+
+template <> struct Wire<POLAR_PROTO_SIMPLE> {
+    static constexpr unsigned long long kPacks = 1;   // packs per wire index (per thread)
+    static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) { return slot_bytes / 16; }
+    static __device__ __forceinline__ void put(const Params&, uint4* slot, unsigned long long k, uint4 v, uint64_t) {
+        st_plain(slot + k, v);
+    }
+    static __device__ __forceinline__ bool get(const Params&, const uint4* slot, unsigned long long k, uint64_t, uint4& v) {
+        v = ld_cg(slot + k);
+        return true;
+    }
+};
+template <> struct Wire<POLAR_PROTO_LL> {
+    static constexpr unsigned long long kPacks = 1;
+    static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) { return slot_bytes / 32; }
+    static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long k, uint4 v, uint64_t f) {
+        jitter(P), st_ll(slot + 2 * k, v.x, v.y, (uint32_t)f);
+        jitter(P), st_ll(slot + 2 * k + 1, v.z, v.w, (uint32_t)f);
+    }
+    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long k, uint64_t f, uint4& v) {
+        uint4 l0, l1;
+        if (!poll_ll(P, slot + 2 * k, (uint32_t)f, l0) || !poll_ll(P, slot + 2 * k + 1, (uint32_t)f, l1)) return false;
+        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+        return true;
+    }
+};
+template <> struct Wire<POLAR_PROTO_LL128> {
+    static constexpr unsigned long long kPacks = kLL128Packs;
+    static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) {
+        return slot_bytes / kLL128UnitBytes;
+    }
+    static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long k, uint4 v, uint64_t f) {
+        jitter(P);
+        __syncwarp();
+        st_ll128(slot + (kLL128UnitBytes / 16) * k, v, f);
+    }
+    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long k, uint64_t f, uint4& v) {
+        __syncwarp();
+        return ld_ll128(P, slot + (kLL128UnitBytes / 16) * k, f, v);
+    }
+};
+
+// Run body(i, j, act) over packs [lo, hi).  Simple / LL: one pack per thread,
+// j = i - lo (the pack's wire index relative to lo).  LL128: one unit of 30
+// packs per warp, j = the unit index relative to lo, i = lo + 30 j + lane; the
+// whole warp runs the body (warp-collective wires) and `act` is false on lanes
+// without a pack.  The body returns false to stop (timeout); so does for_packs.
+template <int PROTO, class Body>
+__device__ __forceinline__ bool for_packs(unsigned long long lo, unsigned long long hi, Body&& body) {
+    if constexpr (PROTO == POLAR_PROTO_LL128) {
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned long long nw = blockDim.x >> 5;
+        for (unsigned long long u = threadIdx.x >> 5; lo + u * kLL128Packs < hi; u += nw) {
+            const unsigned long long i = lo + u * kLL128Packs + lane;
+            if (!body(i, u, lane < (unsigned)kLL128Packs && i < hi)) return false;
+        }
+    } else {
+        for (unsigned long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            if (!body(i, i - lo, true)) return false;
+    }
+    return true;
+}
+
+// staging geometry in whole wire units: packs per wire index for PROTO
+template <int PROTO>
+__device__ __forceinline__ Geo make_geo_for(unsigned long long NP, unsigned long long slot_bytes, int nch, int parts) {
+    using W = Wire<PROTO>;
+    constexpr unsigned long long unit = PROTO == POLAR_PROTO_LL128 ? (unsigned long long)kLL128Packs : kUnit;
+    return make_geo<unit>(NP, W::units(slot_bytes) * W::kPacks, nch, parts);
+}
+
+__device__ __forceinline__ uint4 zero4() { return make_uint4(0, 0, 0, 0); }
+
+// Two-shot LL / LL128: push-based.  RS: rank r writes its part of owner j's
+// shard into j's RS staging slot r; owner polls, reduces in rank order, writes
+// its own buffer and pushes the result into every rank's AG slot; every rank
+// polls the AG slots.  Two NVLink hops, no separate flags.
+
+template <int PROTO>
+__device__ __forceinline__ uint4* ts_stage(const Params& P, int owner, int ag, int par, int slot) {
+    const unsigned long long base = PROTO == POLAR_PROTO_LL128 ? P.ts128_off : P.tsll_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + base + (size_t)ag * 2 * kMaxRanks * 2 * P.tsll_chunk +
                                     ((size_t)(par * kMaxRanks + slot)) * 2 * P.tsll_chunk);
 }
-__device__ __forceinline__ uint4* tsll_ag(const Params& P, int owner, int par, int slot) {
-    return reinterpret_cast<uint4*>(P.scratch[owner] + P.tsll_off + (size_t)2 * kMaxRanks * 2 * P.tsll_chunk +
-                                    ((size_t)(par * kMaxRanks + slot)) * 2 * P.tsll_chunk);
-}
 
-template <int DT, int OP>
+template <int DT, int OP, int PROTO>
 __device__ void twoshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
-    const int n = w.n, tid = w.tid;
+    using W = Wire<PROTO>;
+    const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const Geo g = make_geo(NP, P.tsll_chunk / 16, P.nch, n);
+    const Geo g = make_geo_for<PROTO>(NP, 2 * P.tsll_chunk, P.nch, n);
     char* mine = P.bufs[w.r];
-    bool ok = true;
     for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
-        const uint32_t f = (uint32_t)e;
         const int par = (int)(e & 1);
         unsigned long long lo, hi, off;
+        bool ok = true;
         // RS push: my contribution to every other owner's part
         for (int j = 0; j < n; ++j) {
             if (j == w.r) continue;
             geo_slice(g, NP, k, j, w.c, lo, hi, off);
-            uint4* dst = tsll_rs(P, j, par, w.r) + 2 * off;
-            for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
-                const uint4 v = load_pack<ES>(P, mine, i);
-                uint4* l = dst + 2 * (i - lo);
-                jitter(P), st_ll(l, v.x, v.y, f);
-                jitter(P), st_ll(l + 1, v.z, v.w, f);
-            }
+            uint4* dst = ts_stage<PROTO>(P, j, 0, par, w.r);
+            const unsigned long long ob = off / W::kPacks;
+            for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
+                W::put(P, dst, ob + jj, act ? load_pack<ES>(P, mine, i) : zero4(), e);
+                return true;
+            });
         }
         // reduce my part in rank order, keep it and push it to every rank
         geo_slice(g, NP, k, w.r, w.c, lo, hi, off);
-        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+        const unsigned long long ob = off / W::kPacks;
+        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
             Acc<DT> acc;
-            for (int p = 0; p < n && ok; ++p) {
-                uint4 v;
+            for (int p = 0; p < n; ++p) {
+                uint4 v = zero4();
                 if (p == w.r) {
-                    v = load_pack<ES>(P, mine, i);
-                } else {
-                    const uint4* l = tsll_rs(P, w.r, par, p) + 2 * (off + i - lo);
-                    uint4 l0, l1;
-                    ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
-                    v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+                    if (act) v = load_pack<ES>(P, mine, i);
+                } else if (!W::get(P, ts_stage<PROTO>(P, w.r, 0, par, p), ob + jj, e, v)) {
+                    return false;
                 }
                 if (p == 0) acc_init<DT>(acc, v);
                 else acc_add<DT, OP>(acc, v);
             }
-            if (!ok) break;
             const uint4 out = acc_fin<DT>(acc);
-            store_pack<ES>(P, mine, i, out);
-            for (int p = 0; p < n; ++p) {
-                if (p == w.r) continue;
-                uint4* l = tsll_ag(P, p, par, w.r) + 2 * (off + i - lo);
-                jitter(P), st_ll(l, out.x, out.y, f);
-                jitter(P), st_ll(l + 1, out.z, out.w, f);
-            }
-        }
+            if (act) store_pack<ES>(P, mine, i, out);
+            for (int p = 0; p < n; ++p)
+                if (p != w.r) W::put(P, ts_stage<PROTO>(P, p, 1, par, w.r), ob + jj, out, e);
+            return true;
+        });
         // AG receive: results of every other owner
         for (int j = 0; j < n && ok; ++j) {
             if (j == w.r) continue;
             geo_slice(g, NP, k, j, w.c, lo, hi, off);
-            const uint4* src = tsll_ag(P, w.r, par, j) + 2 * off;
-            for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
-                const uint4* l = src + 2 * (i - lo);
-                uint4 l0, l1;
-                ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
-                if (ok) store_pack<ES>(P, mine, i, make_uint4(l0.x, l0.z, l1.x, l1.z));
-            }
+            const uint4* src = ts_stage<PROTO>(P, w.r, 1, par, j);
+            const unsigned long long obj = off / W::kPacks;
+            ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
+                uint4 v;
+                if (!W::get(P, src, obj + jj, e, v)) return false;
+                if (act) store_pack<ES>(P, mine, i, v);
+                return true;
+            });
         }
         if (!__syncthreads_and(ok)) return;   // parity reuse safety
     }
@@ -431,9 +508,10 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
 __device__ __forceinline__ uint4* os_slot(const Params& P, int owner, int par, int slot) {
     return reinterpret_cast<uint4*>(P.scratch[owner] + P.os_off + ((size_t)(par * kMaxRanks + slot)) * P.os_chunk);
 }
+template <int PROTO>
 __device__ __forceinline__ uint4* osll_slot(const Params& P, int owner, int par, int slot) {
-    return reinterpret_cast<uint4*>(P.scratch[owner] + P.osll_off +
-                                    ((size_t)(par * kMaxRanks + slot)) * 2 * P.osll_chunk);
+    const unsigned long long base = PROTO == POLAR_PROTO_LL128 ? P.os128_off : P.osll_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + base + ((size_t)(par * kMaxRanks + slot)) * 2 * P.osll_chunk);
 }
 
 template <int DT, int OP>
@@ -443,7 +521,7 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const Geo g = make_geo(NP, P.os_chunk / 16, P.nch, 1);
+    const Geo g = make_geo<kUnit>(NP, P.os_chunk / 16, P.nch, 1);
     char* mine = P.bufs[w.r];
     for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
@@ -480,48 +558,45 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
     epoch_publish(P, w, e0 + g.nchunks);
 }
 
-template <int DT, int OP>
+// one-shot LL / LL128: no separate flags; the data carries them
+template <int DT, int OP, int PROTO>
 __device__ void oneshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
-    const int n = w.n, tid = w.tid;
+    using W = Wire<PROTO>;
+    const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
     const unsigned long long NP = npacks<ES>(P);
-    const Geo g = make_geo(NP, P.osll_chunk / 16, P.nch, 1);
+    const Geo g = make_geo_for<PROTO>(NP, 2 * P.osll_chunk, P.nch, 1);
     char* mine = P.bufs[w.r];
     bool ok = true;
     for (unsigned long long k = 0; k < g.nchunks; ++k) {
         const uint64_t e = e0 + k + 1;
-        const uint32_t f = (uint32_t)e;
         const int par = (int)(e & 1);
         unsigned long long lo, hi, off;
         geo_slice(g, NP, k, 0, w.c, lo, hi, off);
-        for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
-            const uint4 v = load_pack<ES>(P, mine, i);
-            for (int p = 0; p < n; ++p) {
-                if (p == w.r) continue;
-                uint4* l = osll_slot(P, p, par, w.r) + 2 * (off + i - lo);
-                jitter(P), st_ll(l, v.x, v.y, f);
-                jitter(P), st_ll(l + 1, v.z, v.w, f);
-            }
-        }
-        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
+        const unsigned long long ob = off / W::kPacks;
+        for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
+            const uint4 v = act ? load_pack<ES>(P, mine, i) : zero4();
+            for (int p = 0; p < n; ++p)
+                if (p != w.r) W::put(P, osll_slot<PROTO>(P, p, par, w.r), ob + j, v, e);
+            return true;
+        });
+        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
             Acc<DT> acc;
-            for (int p = 0; p < n && ok; ++p) {
-                uint4 v;
+            for (int p = 0; p < n; ++p) {
+                uint4 v = zero4();
                 if (p == w.r) {
-                    v = load_pack<ES>(P, mine, i);
-                } else {
-                    const uint4* l = osll_slot(P, w.r, par, p) + 2 * (off + i - lo);
-                    uint4 l0, l1;
-                    ok = poll_ll(P, l, f, l0) && poll_ll(P, l + 1, f, l1);
-                    v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+                    if (act) v = load_pack<ES>(P, mine, i);
+                } else if (!W::get(P, osll_slot<PROTO>(P, w.r, par, p), ob + j, e, v)) {
+                    return false;
                 }
                 if (p == 0) acc_init<DT>(acc, v);
                 else acc_add<DT, OP>(acc, v);
             }
-            if (ok) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
-        }
+            if (act) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+            return true;
+        });
         if (!__syncthreads_and(ok)) return;   // parity reuse safety
     }
     epoch_publish(P, w, e0 + g.nchunks);
@@ -533,34 +608,16 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
 // owners' ChanState across calls, so FIFOs never need resetting.
 //   Simple: payload, fence, tail flag (= sent) in the receiver's scratch.
 //   LL    : payload as LL lines whose flag is (u32)(slot sequence + 1).
-//   Both  : the receiver returns a head credit (= consumed) to the sender.
+//   LL128 : payload as LL128 line groups whose flag is slot sequence + 1.
+//   All   : the receiver returns a head credit (= consumed) to the sender.
+// The three protocols share the counters and flags but not the FIFO memory.
 
-template <int PROTO> struct Fifo;
-
-template <> struct Fifo<POLAR_PROTO_SIMPLE> {
-    // wire packs per slot for `wp` 16-B packs per element-pack
-    static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 16; }
-    static __device__ __forceinline__ void put(const Params&, uint4* slot, unsigned long long j, uint4 v, uint32_t) {
-        st_plain(slot + j, v);
-    }
-    static __device__ __forceinline__ bool get(const Params&, const uint4* slot, unsigned long long j, uint32_t, uint4& v) {
-        v = ld_cg(slot + j);
-        return true;
-    }
-};
-template <> struct Fifo<POLAR_PROTO_LL> {
-    static __device__ __forceinline__ unsigned long long slot_packs(unsigned long long slot_bytes) { return slot_bytes / 32; }
-    static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long j, uint4 v, uint32_t f) {
-        jitter(P), st_ll(slot + 2 * j, v.x, v.y, f);
-        jitter(P), st_ll(slot + 2 * j + 1, v.z, v.w, f);
-    }
-    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long j, uint32_t f, uint4& v) {
-        uint4 l0, l1;
-        if (!poll_ll(P, slot + 2 * j, f, l0) || !poll_ll(P, slot + 2 * j + 1, f, l1)) return false;
-        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
-        return true;
-    }
-};
+template <int PROTO> __device__ __forceinline__ unsigned long long ring_slot_bytes(const Params& P) {
+    return PROTO == POLAR_PROTO_LL ? P.ringll_slot : PROTO == POLAR_PROTO_LL128 ? P.ring128_slot : P.ring_slot;
+}
+template <int PROTO> __device__ __forceinline__ unsigned long long tree_slot_bytes(const Params& P) {
+    return PROTO == POLAR_PROTO_LL ? P.treell_slot : PROTO == POLAR_PROTO_LL128 ? P.tree128_slot : P.tree_slot;
+}
 
 // ======================================================================= ring
 // nch rings in rank order.  Per channel, loop chunks of n sub-chunks; step s of
@@ -569,23 +626,22 @@ template <> struct Fifo<POLAR_PROTO_LL> {
 
 template <int PROTO>
 __device__ __forceinline__ uint4* ring_slot(const Params& P, int owner, int c, unsigned long long seq) {
-    const bool ll = PROTO == POLAR_PROTO_LL;
-    const unsigned long long slot = ll ? P.ringll_slot : P.ring_slot;
-    const unsigned long long off = ll ? P.ringll_off : P.ring_off;
-    return reinterpret_cast<uint4*>(P.scratch[owner] + off + ((size_t)c * kSteps + (seq % kSteps)) * slot);
+    const unsigned long long off =
+        PROTO == POLAR_PROTO_LL ? P.ringll_off : PROTO == POLAR_PROTO_LL128 ? P.ring128_off : P.ring_off;
+    return reinterpret_cast<uint4*>(P.scratch[owner] + off + ((size_t)c * kSteps + (seq % kSteps)) * ring_slot_bytes<PROTO>(P));
 }
 
 template <int DT, int OP, int PROTO>
 __device__ void ring(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int AW = AccWords<DT>::N;
-    using F = Fifo<PROTO>;
+    using W = Wire<PROTO>;
     const int n = w.n, tid = w.tid, r = w.r, c = w.c;
     const int next = (r + 1) % n, prev = (r + n - 1) % n;
     ChanState* st = chan_state(P, r, c);
     unsigned long long sent = st->ring_sent, recvd = st->ring_recv;
-    const unsigned long long slot_bytes = PROTO == POLAR_PROTO_LL ? P.ringll_slot : P.ring_slot;
-    const unsigned long long SP = F::slot_packs(slot_bytes) / AW;   // element-packs per slot
+    // element packs per slot: AW wire indices per pack (f32 partials of bf16)
+    const unsigned long long SP = W::units(ring_slot_bytes<PROTO>(P)) / AW * W::kPacks;
     const unsigned long long NP = npacks<ES>(P);
     unsigned long long ca, cb;
     split_range(0, NP, P.nch, c, ca, cb);
@@ -616,36 +672,35 @@ __device__ void ring(const Params& P, const Who& w) {
             if (!__syncthreads_and(ok)) return;
             const uint4* src = ring_slot<PROTO>(P, r, c, recvd);
             uint4* dst = ring_slot<PROTO>(P, next, c, sent);
-            const uint32_t fin = (uint32_t)(recvd + 1), fout = (uint32_t)(sent + 1);
-            for (unsigned long long i = ks + tid; i < ke && ok; i += blockDim.x) {
-                const unsigned long long j = i - ks;
+            const uint64_t fin = recvd + 1, fout = sent + 1;
+            ok = for_packs<PROTO>(ks, ke, [&](unsigned long long i, unsigned long long j, bool act) {
                 if (s == 0) {
                     Acc<DT> acc;
-                    acc_init<DT>(acc, load_pack<ES>(P, mine, i));
+                    acc_init<DT>(acc, act ? load_pack<ES>(P, mine, i) : zero4());
 #pragma unroll
-                    for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
+                    for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
                 } else if (s < n) {
                     Acc<DT> acc;
 #pragma unroll
-                    for (int q = 0; q < AW; ++q) ok = ok && F::get(P, src, j * AW + q, fin, acc.w[q]);
-                    if (!ok) break;
-                    acc_add<DT, OP>(acc, load_pack<ES>(P, mine, i));
+                    for (int q = 0; q < AW; ++q)
+                        if (!W::get(P, src, j * AW + q, fin, acc.w[q])) return false;
+                    if (act) acc_add<DT, OP>(acc, load_pack<ES>(P, mine, i));
                     if (s < n - 1) {
 #pragma unroll
-                        for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
+                        for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
                     } else {
                         const uint4 out = acc_fin<DT>(acc);
-                        store_pack<ES>(P, mine, i, out);
-                        F::put(P, dst, j, out, fout);
+                        if (act) store_pack<ES>(P, mine, i, out);
+                        W::put(P, dst, j, out, fout);
                     }
                 } else {
                     uint4 v;
-                    ok = F::get(P, src, j, fin, v);
-                    if (!ok) break;
-                    store_pack<ES>(P, mine, i, v);
-                    if (do_send) F::put(P, dst, j, v, fout);
+                    if (!W::get(P, src, j, fin, v)) return false;
+                    if (act) store_pack<ES>(P, mine, i, v);
+                    if (do_send) W::put(P, dst, j, v, fout);
                 }
-            }
+                return true;
+            });
             if (!__syncthreads_and(ok)) return;
             if (tid == 0) {
                 if (do_send && PROTO == POLAR_PROTO_SIMPLE) {
@@ -671,26 +726,28 @@ __device__ void ring(const Params& P, const Who& w) {
 // rounds once and stores.  Down phase: the result flows back down.
 
 template <int PROTO>
+__device__ __forceinline__ char* tree_base(const Params& P, int owner) {
+    const unsigned long long off =
+        PROTO == POLAR_PROTO_LL ? P.treell_off : PROTO == POLAR_PROTO_LL128 ? P.tree128_off : P.tree_off;
+    return P.scratch[owner] + off;
+}
+template <int PROTO>
 __device__ __forceinline__ uint4* tree_up_slot(const Params& P, int owner, int c, int child, unsigned long long seq) {
-    const bool ll = PROTO == POLAR_PROTO_LL;
-    const unsigned long long slot = ll ? P.treell_slot : P.tree_slot;
-    const unsigned long long off = ll ? P.treell_off : P.tree_off;
-    return reinterpret_cast<uint4*>(P.scratch[owner] + off + (((size_t)c * 2 + child) * kSteps + (seq % kSteps)) * slot);
+    return reinterpret_cast<uint4*>(tree_base<PROTO>(P, owner) +
+                                    (((size_t)c * 2 + child) * kSteps + (seq % kSteps)) * tree_slot_bytes<PROTO>(P));
 }
 template <int PROTO>
 __device__ __forceinline__ uint4* tree_dn_slot(const Params& P, int owner, int c, unsigned long long seq) {
-    const bool ll = PROTO == POLAR_PROTO_LL;
-    const unsigned long long slot = ll ? P.treell_slot : P.tree_slot;
-    const unsigned long long off = ll ? P.treell_off : P.tree_off;
-    return reinterpret_cast<uint4*>(P.scratch[owner] + off +
-                                    ((size_t)kMaxCh * 2 * kSteps + (size_t)c * kSteps + (seq % kSteps)) * slot);
+    return reinterpret_cast<uint4*>(tree_base<PROTO>(P, owner) +
+                                    ((size_t)kMaxCh * 2 * kSteps + (size_t)c * kSteps + (seq % kSteps)) *
+                                        tree_slot_bytes<PROTO>(P));
 }
 
 template <int DT, int OP, int PROTO>
 __device__ void tree(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int AW = AccWords<DT>::N;
-    using F = Fifo<PROTO>;
+    using W = Wire<PROTO>;
     const int n = w.n, tid = w.tid, r = w.r, c = w.c;
     const int pos = ((r - c) % n + n) % n;
     auto rank_of = [&](int q) { return (q + c) % n; };
@@ -705,8 +762,7 @@ __device__ void tree(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, r, c);
     unsigned long long usent = st->tree_usent, dsent = st->tree_dsent, drecv = st->tree_drecv;
     unsigned long long urecv[2] = {st->tree_urecv[0], st->tree_urecv[1]};
-    const unsigned long long slot_bytes = PROTO == POLAR_PROTO_LL ? P.treell_slot : P.tree_slot;
-    const unsigned long long SP = F::slot_packs(slot_bytes) / AW;
+    const unsigned long long SP = W::units(tree_slot_bytes<PROTO>(P)) / AW * W::kPacks;
     const unsigned long long NP = npacks<ES>(P);
     unsigned long long ca, cb;
     split_range(0, NP, P.nch, c, ca, cb);
@@ -726,26 +782,26 @@ __device__ void tree(const Params& P, const Who& w) {
         }
         if (!__syncthreads_and(ok)) return;
         uint4* dst = root ? nullptr : tree_up_slot<PROTO>(P, parent, c, my_child_idx, usent);
-        const uint32_t fout = (uint32_t)(usent + 1);
-        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
-            const unsigned long long j = i - lo;
+        const uint64_t fout = usent + 1;
+        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
             Acc<DT> acc;
-            acc_init<DT>(acc, load_pack<ES>(P, mine, i));
-            for (int k = 0; k < nchild && ok; ++k) {
+            acc_init<DT>(acc, act ? load_pack<ES>(P, mine, i) : zero4());
+            for (int k = 0; k < nchild; ++k) {
                 const uint4* src = tree_up_slot<PROTO>(P, r, c, k, urecv[k]);
                 Acc<DT> b;
 #pragma unroll
-                for (int q = 0; q < AW; ++q) ok = ok && F::get(P, src, j * AW + q, (uint32_t)(urecv[k] + 1), b.w[q]);
-                if (ok) acc_merge<DT, OP>(acc, b);
+                for (int q = 0; q < AW; ++q)
+                    if (!W::get(P, src, j * AW + q, urecv[k] + 1, b.w[q])) return false;
+                acc_merge<DT, OP>(acc, b);
             }
-            if (!ok) break;
             if (root) {
-                store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+                if (act) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
             } else {
 #pragma unroll
-                for (int q = 0; q < AW; ++q) F::put(P, dst, j * AW + q, acc.w[q], fout);
+                for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
             }
-        }
+            return true;
+        });
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (!root && PROTO == POLAR_PROTO_SIMPLE) {
@@ -769,19 +825,18 @@ __device__ void tree(const Params& P, const Who& w) {
         }
         if (!__syncthreads_and(ok)) return;
         const uint4* src = root ? nullptr : tree_dn_slot<PROTO>(P, r, c, drecv);
-        const uint32_t fin = (uint32_t)(drecv + 1), fout = (uint32_t)(dsent + 1);
-        for (unsigned long long i = lo + tid; i < hi && ok; i += blockDim.x) {
-            const unsigned long long j = i - lo;
-            uint4 v;
+        const uint64_t fin = drecv + 1, fout = dsent + 1;
+        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
+            uint4 v = zero4();
             if (root) {
-                v = load_pack<ES>(P, mine, i);
+                if (act) v = load_pack<ES>(P, mine, i);
             } else {
-                ok = F::get(P, src, j, fin, v);
-                if (!ok) break;
-                store_pack<ES>(P, mine, i, v);
+                if (!W::get(P, src, j, fin, v)) return false;
+                if (act) store_pack<ES>(P, mine, i, v);
             }
-            for (int k = 0; k < nchild; ++k) F::put(P, tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
-        }
+            for (int k = 0; k < nchild; ++k) W::put(P, tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
+            return true;
+        });
         if (!__syncthreads_and(ok)) return;
         if (tid == 0) {
             if (PROTO == POLAR_PROTO_SIMPLE && nchild) {
@@ -818,10 +873,10 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
     const unsigned long long tel_t0 = tel ? globaltimer() : 0;
     if constexpr (ALGO == POLAR_ALGO_TWOSHOT) {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) twoshot_simple<DT, OP>(P, w);
-        else twoshot_ll<DT, OP>(P, w);
+        else twoshot_ll<DT, OP, PROTO>(P, w);
     } else if constexpr (ALGO == POLAR_ALGO_ONESHOT) {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) oneshot_simple<DT, OP>(P, w);
-        else oneshot_ll<DT, OP>(P, w);
+        else oneshot_ll<DT, OP, PROTO>(P, w);
     } else if constexpr (ALGO == POLAR_ALGO_RING) {
         ring<DT, OP, PROTO>(P, w);
     } else {

@@ -58,6 +58,10 @@ struct Layout {
     size_t ringll_off, ringll_slot;   // ring LL FIFO: [kMaxCh][kSteps][2*ringll_slot]
     size_t tree_off, tree_slot;       // tree Simple: up [kMaxCh][2][kSteps][slot], down [kMaxCh][kSteps][slot]
     size_t treell_off, treell_slot;   // tree LL: same with 2x
+    size_t os128_off;                 // one-shot LL128: [2][kMaxRanks][2*osll_chunk] (same wire bytes as LL)
+    size_t ts128_off;                 // two-shot LL128: RS + AG, as two-shot LL
+    size_t ring128_off, ring128_slot; // ring LL128 FIFO: [kMaxCh][kSteps][ring128_slot] (wire bytes)
+    size_t tree128_off, tree128_slot; // tree LL128: up [kMaxCh][2][kSteps], down [kMaxCh][kSteps]
     size_t bounce_off, bounce_bytes;  // two-shot bounce for unregistered buffers (real comms)
     size_t total;
 };

@@ -71,8 +71,7 @@ polar_status validate_rows(const polar_policy_row* rows, uint32_t nrows) {
             default: return POLAR_EINVAL;
         }
         switch (r.proto) {
-            case POLAR_PROTO_LL: case POLAR_PROTO_SIMPLE: case POLAR_UNSET: break;
-            case POLAR_PROTO_LL128: unsupported = true; break;
+            case POLAR_PROTO_LL: case POLAR_PROTO_LL128: case POLAR_PROTO_SIMPLE: case POLAR_UNSET: break;
             default: return POLAR_EINVAL;
         }
         // strictly ascending max_bytes within the (coll, nranks) group
@@ -162,7 +161,7 @@ const char* polar_status_string(polar_status s) {
         case POLAR_OK: return "POLAR_OK";
         case POLAR_EINVAL: return "POLAR_EINVAL: invalid argument or policy table";
         case POLAR_ECUDA: return "POLAR_ECUDA: CUDA call failed";
-        case POLAR_EUNSUPPORTED: return "POLAR_EUNSUPPORTED: not built (NVLS/LL128/other collectives)";
+        case POLAR_EUNSUPPORTED: return "POLAR_EUNSUPPORTED: not built (NVLS, or an algorithm/protocol a collective has no kernel for)";
         case POLAR_ETIMEOUT: return "POLAR_ETIMEOUT: device wait for a peer timed out";
         case POLAR_EBUSY: return "POLAR_EBUSY: object in use";
         case POLAR_ESTATE: return "POLAR_ESTATE: comm unusable";

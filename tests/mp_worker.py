@@ -58,7 +58,7 @@ def main():
         results.append({"tag": tag, "rank": rank, "ok": bool(ok), "identical": len(set(hs)) == 1})
 
     for algo in ("oneshot", "twoshot", "ring", "tree"):
-        for proto in ("ll", "simple"):
+        for proto in ("ll", "ll128", "simple"):
             for dtype, count, nch in (("f32", 70_001, 3), ("bf16", 5_003, 2), ("i32", 1, 1)):
                 xs = synth.gen_ranks(dtype, count, ws, cfg=31, dist="ints")
                 t = to_device(xs[rank], dtype)

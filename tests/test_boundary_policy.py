@@ -96,11 +96,21 @@ def test_spec_blocks_match_oracle():
         _compare(rows)
 
 
-def test_nvlink_ring_mid_v2_rejected_and_old_kept():
+def test_nvlink_ring_mid_v2_accepted():
     rows, _, status = rows_and_cases("nvlink_ring_mid_v2.txt")
     g0 = L.generation()
+    st, gen = L.set_policy_status(rows)
+    assert L.STATUS_NAMES[st] == status == "ok"
+    assert gen == g0 + 1
+    _compare(rows)
+
+
+def test_nvls_rejected_and_old_kept():
+    rows = [(0, 0, 1 << 20, OP.RING, OP.LL128, 4), (0, 0, 1 << 30, OP.NVLS, OP.SIMPLE, 0)]
+    L.set_policy([])
+    g0 = L.generation()
     st, _ = L.set_policy_status(rows)
-    assert L.STATUS_NAMES[st] == status == "eunsupported"
+    assert L.STATUS_NAMES[st] == "eunsupported"
     assert L.generation() == g0
     _compare([])
 
@@ -189,6 +199,6 @@ def test_committed_policy_files_validate():
         exp = OP.validate(rows)
         st, _ = L.set_policy_status(rows)
         assert L.STATUS_NAMES[st] == exp, name
-        assert exp == ("eunsupported" if name == "nvlink_ring_mid_v2.json" else "ok"), name
+        assert exp == "ok", name
         if exp == "ok":
             _compare(rows)

@@ -10,9 +10,12 @@ from paper_2603_11438_b200 import polar as L
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_validate_and_reject(capsys):
+def test_validate_and_reject(capsys, tmp_path):
     assert cli.main(["validate", os.path.join(ROOT, "policies", "b200_virtual8.json")]) == 0
-    assert cli.main(["validate", os.path.join(ROOT, "policies", "nvlink_ring_mid_v2.json")]) == 3
+    assert cli.main(["validate", os.path.join(ROOT, "policies", "nvlink_ring_mid_v2.json")]) == 0
+    nvls = tmp_path / "nvls.json"
+    nvls.write_text(json.dumps({"name": "nvls", "rows": [[0, 0, 1 << 30, 2, 2, 0]]}))
+    assert cli.main(["validate", str(nvls)]) == 3
     assert "eunsupported" in capsys.readouterr().out
     L.set_policy([])
 
@@ -39,7 +42,7 @@ def test_reload_and_adaptive(capsys):
     L.set_policy([])
 
 
-def test_polar_policy_env_loads_table():
+def test_polar_policy_env_loads_table(tmp_path):
     env = dict(os.environ)
     env["POLAR_POLICY"] = os.path.join(ROOT, "policies", "bad_channels.json")
     code = ("from paper_2603_11438_b200 import polar as L; d = L.decide(8, 1 << 27); "
@@ -47,6 +50,8 @@ def test_polar_policy_env_loads_table():
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert r.stdout.split() == ["1", "1"]
-    env["POLAR_POLICY"] = os.path.join(ROOT, "policies", "nvlink_ring_mid_v2.json")
+    nvls = tmp_path / "nvls.json"
+    nvls.write_text(json.dumps({"name": "nvls", "rows": [[0, 0, 1 << 30, 2, 2, 0]]}))
+    env["POLAR_POLICY"] = str(nvls)
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode != 0 and "EUNSUPPORTED" in r.stderr

@@ -28,7 +28,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 from paper_2603_11438_b200 import polar as L  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-COMBOS = list(itertools.product(["oneshot", "twoshot", "ring", "tree"], ["ll", "simple"]))
+COMBOS = list(itertools.product(["oneshot", "twoshot", "ring", "tree"], ["ll", "ll128", "simple"]))
 
 
 @pytest.mark.parametrize("n", [3, 8])

@@ -23,7 +23,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 from paper_2603_11438_b200 import polar as L  # noqa: E402
 
 ALGOS = ["oneshot", "twoshot", "ring", "tree"]
-PROTOS = ["ll", "simple"]
+PROTOS = ["ll", "ll128", "simple"]
 _COMMS = {}
 
 
@@ -205,3 +205,51 @@ def test_twoshot_tma_auto_large_n2():
         exp = orc.allreduce([x[lo:hi] for x in xs], "f32", "sum")
         for t in ts:
             assert np.array_equal(to_host(t[lo:hi], "f32").view(np.uint32), exp.view(np.uint32))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_ll128_stress_back_to_back(algo):
+    """LL128 relies on a warp's 128-B line store landing as one unit (device.cuh
+    "LL128"): many back-to-back calls of one size, no host sync in between,
+    integer-valued inputs so every algorithm must be bit-exact; a torn line
+    (flag seen before its data) would show up as a wrong element."""
+    from oracle import allreduce as orc
+    n, dtype, count = 8, "f32", 1_000_003
+    c = comm(n)
+    cases = []
+    for it in range(12):
+        xs = synth.gen_ranks(dtype, count, n, cfg=300 + it, dist="ints")
+        ts = [to_device(x, dtype) for x in xs]
+        c.allreduce_forced(ts, algo, "ll128", 1 + (it * 5) % 32)
+        cases.append((xs, ts))
+    torch.cuda.synchronize()
+    c.check()
+    for xs, ts in cases:
+        exp = orc.allreduce(xs, dtype, "sum")
+        for t in ts:
+            assert np.array_equal(to_host(t, dtype), exp)
+
+
+def test_paper_policy_nvlink_ring_mid_v2():
+    """The paper's case-study policy as a table: Ring/LL128 at
+    4-32 MiB, Ring/Simple at 64-192 MiB, default otherwise; 8 ranks, f32 sum."""
+    from oracle import allreduce as orc
+    from tests.golden_io import rows_and_cases
+    rows, _, _ = rows_and_cases("nvlink_ring_mid_v2.txt")
+    L.set_policy(rows)
+    try:
+        n = 8
+        c = comm(n)
+        for nbytes in (2 << 20, 4 << 20, 8 << 20, 32 << 20, 48 << 20, 64 << 20):
+            count = nbytes // 4
+            xs = synth.gen_ranks("f32", count, n, cfg=21, dist="ints")
+            ts = [to_device(x, "f32") for x in xs]
+            c.allreduce(ts)
+            torch.cuda.synchronize()
+            c.check()
+            assert c.last_decision().as_tuple() == OP.decide(rows, 0, n, nbytes)
+            exp = orc.allreduce(xs, "f32", "sum")
+            for t in ts:
+                assert np.array_equal(to_host(t, "f32"), exp)
+    finally:
+        L.set_policy([])

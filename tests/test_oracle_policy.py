@@ -22,7 +22,7 @@ def test_listing1_threshold_cases():
 
 def test_nvlink_ring_mid_v2_cases():
     rows, cases, status = rows_and_cases("nvlink_ring_mid_v2.txt")
-    assert P.validate(rows) == status == "eunsupported"
+    assert P.validate(rows) == status == "ok"
     for case in cases:
         nranks, nbytes = case[0], case[1]
         got = P.decide(rows, P.COLL_ALLREDUCE, nranks, nbytes)
@@ -83,7 +83,7 @@ def test_validation_rules():
     assert P.validate([(9, 0, 100, P.RING, P.LL, 4)]) == "einval" # unknown coll
     assert P.validate([(0, 9, 100, P.RING, P.LL, 4)]) == "einval" # nranks > 8
     assert P.validate([(0, 0, 100, P.NVLS, P.SIMPLE, 4)]) == "eunsupported"
-    assert P.validate([(0, 0, 100, P.RING, P.LL128, 4)]) == "eunsupported"
+    assert P.validate([(0, 0, 100, P.RING, P.LL128, 4)]) == "ok"            # LL128 built (f2)
     assert P.validate([(0, 0, 100, P.NVLS, P.SIMPLE, 4), ok]) == "einval"
     assert P.validate([(0, 0, i, P.RING, P.LL, 1) for i in range(65)]) == "einval"
     assert P.validate([(0, 0, i, P.RING, P.LL, 1) for i in range(64)]) == "ok"
