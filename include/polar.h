@@ -244,10 +244,15 @@ polar_status polar_allreduce_forced(polar_comm_t comm, void* const* bufs, size_t
                                     polar_dtype dtype, polar_op op, const polar_decision* forced,
                                     void* stream);
 
-/* End-to-end form over HOST memory: host_bufs[nlocal] (pinned or pageable) are
- * copied to the device buffers dev_bufs[nlocal], reduced in place, and the
- * result is copied back into host_bufs; synchronous (returns after the D2H
- * copy completed).  Used for the bench's e2e number. */
+/* End-to-end form over HOST memory: host_bufs[nlocal] (pinned for overlap;
+ * pageable works but serialises) are copied to the device buffers
+ * dev_bufs[nlocal], reduced in place, and the result is copied back into
+ * host_bufs; synchronous (returns after the last D2H copy completed).  The
+ * message is processed in chunks of POLAR_HOST_CHUNK bytes per rank (default
+ * 8 MiB): the H2D copy of chunk k+1, the AllReduce of chunk k (one decision and
+ * one launch per chunk, on `stream`) and the D2H copy of chunk k-1 overlap on
+ * two library-owned copy streams.  Chunking does not change the result (the
+ * reduction is elementwise).  Used for the bench's e2e number. */
 polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, void* const* dev_bufs,
                                   size_t count, polar_dtype dtype, polar_op op, void* stream);
 

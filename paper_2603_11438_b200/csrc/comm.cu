@@ -123,6 +123,9 @@ struct polar_comm_s {
     unsigned long long tel_consumed = 0; // samples consumed up to (and including) this seq
     int tma_mode = 2;                    // two-shot Simple via TMA smem staging: 0 never, 1 always, 2 auto
     unsigned long long timeout_ns = 0;
+    // polar_allreduce_host chunk pipeline (created on first use)
+    cudaStream_t hs_in = nullptr, hs_out = nullptr;
+    cudaEvent_t he_start = nullptr, he_in = nullptr, he_red = nullptr, he_out = nullptr;
     std::mutex mu;
 };
 
@@ -318,6 +321,10 @@ void destroy_comm(polar_comm_s* c, bool collective) {
         if (c->scratch_own[p]) cudaFree(c->scratch_own[p]);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->tel_host) cudaFreeHost(c->tel_host);
+    if (c->hs_in) cudaStreamDestroy(c->hs_in);
+    if (c->hs_out) cudaStreamDestroy(c->hs_out);
+    for (cudaEvent_t e : {c->he_start, c->he_in, c->he_red, c->he_out})
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 
@@ -859,13 +866,50 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     DeviceGuard dg(comm->device);
     if (!dg.ok) return POLAR_ECUDA;
-    const size_t bytes = count * (size_t)es;
-    for (int l = 0; l < comm->nlocal && count; ++l)
-        CU_TRY(cudaMemcpyAsync(dev_bufs[l], host_bufs[l], bytes, cudaMemcpyHostToDevice, s));
-    polar_status st = do_allreduce(comm, dev_bufs, count, dtype, op, nullptr, s);
-    if (st != POLAR_OK) return st;
-    for (int l = 0; l < comm->nlocal && count; ++l)
-        CU_TRY(cudaMemcpyAsync(host_bufs[l], dev_bufs[l], bytes, cudaMemcpyDeviceToHost, s));
+    if (count == 0) return do_allreduce(comm, dev_bufs, 0, dtype, op, nullptr, s);
+    // Chunk pipeline: H2D of chunk k+1 (copy stream in), the AllReduce of chunk k
+    // (the caller's stream) and D2H of chunk k-1 (copy stream out) overlap, so the
+    // two PCIe directions run concurrently.  Each chunk is an independent
+    // AllReduce of a contiguous element range (decided by its own bytes); the
+    // result is the AllReduce of the whole message because the op is elementwise.
+    if (!comm->hs_in) {
+        CU_TRY(cudaStreamCreateWithFlags(&comm->hs_in, cudaStreamNonBlocking));
+        CU_TRY(cudaStreamCreateWithFlags(&comm->hs_out, cudaStreamNonBlocking));
+        CU_TRY(cudaEventCreateWithFlags(&comm->he_start, cudaEventDisableTiming));
+        CU_TRY(cudaEventCreateWithFlags(&comm->he_in, cudaEventDisableTiming));
+        CU_TRY(cudaEventCreateWithFlags(&comm->he_red, cudaEventDisableTiming));
+        CU_TRY(cudaEventCreateWithFlags(&comm->he_out, cudaEventDisableTiming));
+    }
+    const size_t chunk_bytes = env_size("POLAR_HOST_CHUNK", 8u << 20);
+    size_t chunk = std::max<size_t>(1, chunk_bytes / (size_t)es);
+    chunk = std::max<size_t>(16 / es, chunk / (16 / es) * (16 / es));   // keep chunk starts 16-B aligned
+    CU_TRY(cudaEventRecord(comm->he_start, s));
+    CU_TRY(cudaStreamWaitEvent(comm->hs_in, comm->he_start, 0));
+    CU_TRY(cudaStreamWaitEvent(comm->hs_out, comm->he_start, 0));
+    std::vector<void*> sub(comm->nlocal);
+    for (size_t done = 0; done < count; done += chunk) {
+        const size_t n = std::min(chunk, count - done);
+        const size_t off = done * (size_t)es, nb = n * (size_t)es;
+        for (int l = 0; l < comm->nlocal; ++l)
+            CU_TRY(cudaMemcpyAsync(static_cast<char*>(dev_bufs[l]) + off, static_cast<const char*>(host_bufs[l]) + off,
+                                   nb, cudaMemcpyHostToDevice, comm->hs_in));
+        CU_TRY(cudaEventRecord(comm->he_in, comm->hs_in));
+        CU_TRY(cudaStreamWaitEvent(s, comm->he_in, 0));
+        for (int l = 0; l < comm->nlocal; ++l) sub[l] = static_cast<char*>(dev_bufs[l]) + off;
+        polar_status st = do_allreduce(comm, sub.data(), n, dtype, op, nullptr, s);
+        if (st != POLAR_OK) {
+            cudaStreamSynchronize(comm->hs_in);
+            cudaStreamSynchronize(comm->hs_out);
+            return st;
+        }
+        CU_TRY(cudaEventRecord(comm->he_red, s));
+        CU_TRY(cudaStreamWaitEvent(comm->hs_out, comm->he_red, 0));
+        for (int l = 0; l < comm->nlocal; ++l)
+            CU_TRY(cudaMemcpyAsync(static_cast<char*>(host_bufs[l]) + off, static_cast<char*>(dev_bufs[l]) + off, nb,
+                                   cudaMemcpyDeviceToHost, comm->hs_out));
+    }
+    CU_TRY(cudaEventRecord(comm->he_out, comm->hs_out));
+    CU_TRY(cudaStreamWaitEvent(s, comm->he_out, 0));
     CU_TRY(cudaStreamSynchronize(s));
     return check_latched(comm);
 }

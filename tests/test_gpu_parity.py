@@ -253,3 +253,27 @@ def test_paper_policy_nvlink_ring_mid_v2():
                 assert np.array_equal(to_host(t, "f32"), exp)
     finally:
         L.set_policy([])
+
+
+@pytest.mark.parametrize("chunk", ["65536", "8388608"])
+def test_allreduce_host_chunk_pipeline(chunk, monkeypatch):
+    """polar_allreduce_host (the e2e path): host buffers in, host buffers out,
+    processed as overlapping chunks; ragged counts spanning many chunks, pinned
+    and pageable host memory, and the policy-selected kernels per chunk."""
+    from oracle import allreduce as orc
+    monkeypatch.setenv("POLAR_HOST_CHUNK", chunk)
+    for n, dtype, count in ((8, "f32", 3_000_017), (3, "bf16", 1_000_001), (2, "i64", 70_001)):
+        xs = synth.gen_ranks(dtype, count, n, cfg=41, dist=default_dist(dtype))
+        c = comm(n)
+        for pinned in (True, False):
+            host = [torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16) if dtype == "bf16"
+                    else torch.from_numpy(x.copy()) for x in xs]
+            if pinned:
+                host = [h.pin_memory() for h in host]
+            dev = [torch.empty_like(h, device="cuda") for h in host]
+            c.allreduce_host(host, dev)
+            c.check()
+            exp = orc.allreduce(xs, dtype, "sum")
+            for h in host:
+                got = h.view(torch.int16).numpy() if dtype == "bf16" else h.numpy()
+                assert np.array_equal(got.view(np.uint8), exp.view(np.uint8))
