@@ -361,6 +361,19 @@ polar_status polar_adaptive_simulate(const polar_adaptive_params* params, uint32
 const char* polar_status_string(polar_status s);
 
 /* Library build tag, e.g. "polar 0.1 sm_100a". */
+/* Hardware probe of the LL128 premise: `pairs` writer /
+ * reader warp pairs on `cuda_device` stream `iters` LL128 line groups each
+ * through an 8-group FIFO (writer: the product's st_ll128 after an optional
+ * random delay < jitter_ns, drawn per lane (jitter_mode 0, the product's fault
+ * injection), once per warp (jitter_mode 1) or as a per-lane divergent busy
+ * wait without NANOSLEEP (jitter_mode 2); reader: the product's poll
+ * pattern) and count reader
+ * lanes whose payload does not match the sequence number the line flags
+ * announced.  *torn_lanes == 0 is the premise; *lane_reads = lanes checked.
+ * Synchronous; allocates and frees its own device memory.  Diagnostic only. */
+polar_status polar_probe_ll128(int cuda_device, int pairs, unsigned long long iters, unsigned jitter_ns,
+                               int jitter_mode, unsigned long long* torn_lanes, unsigned long long* lane_reads);
+
 const char* polar_version(void);
 
 #ifdef __cplusplus

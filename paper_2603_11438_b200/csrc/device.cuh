@@ -142,11 +142,13 @@ __device__ __forceinline__ void st_ll128(uint4* group, uint4 v, uint64_t flag) {
     w.y = __shfl_sync(0xffffffffu, v.y, src);
     w.z = __shfl_sync(0xffffffffu, v.z, src);
     w.w = __shfl_sync(0xffffffffu, v.w, src);
-    if (q == 7) {
-        if (g & 1) { w.x = w.z; w.y = w.w; }
-        w.z = (uint32_t)flag;
-        w.w = (uint32_t)(flag >> 32);
-    }
+    // flag lane: its half of pack 28 + g/2 in the low 8 B, the flag in the high 8 B
+    // (selects, not branches: the store below must be issued by the whole warp)
+    const bool fl = q == 7, hi = (g & 1) != 0;
+    w.x = fl && hi ? w.z : w.x;
+    w.y = fl && hi ? w.w : w.y;
+    w.z = fl ? (uint32_t)flag : w.z;
+    w.w = fl ? (uint32_t)(flag >> 32) : w.w;
     asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(group + lane), "r"(w.x), "r"(w.y), "r"(w.z),
                  "r"(w.w)
                  : "memory");
@@ -207,7 +209,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // Fault injection: delay a random 1/8 of the signalling stores so
-// that every protocol is exercised under skewed arrival orders.
+// that every protocol is exercised under skewed arrival orders.  jitter() draws
+// per thread (LL lines and flags are per-thread stores); jitter_warp() draws
+// once per warp, for LL128, whose premise is a CONVERGENT warp store: per-lane
+// NANOSLEEP delays right before the store were measured to split it and tear
+// lines (polar_probe_ll128, profiles/r01_probe_ll128.jsonl).
 __device__ __forceinline__ void jitter(const Params& P) {
     if (P.jitter_ns == 0) return;
     uint32_t x = (uint32_t)globaltimer() * 2654435761u ^ (threadIdx.x * 40503u) ^ (blockIdx.x * 2246822519u);
@@ -215,6 +221,17 @@ __device__ __forceinline__ void jitter(const Params& P) {
     x *= 2246822519u;
     x ^= x >> 13;
     if ((x & 7u) == 0) __nanosleep(x % P.jitter_ns);
+}
+
+__device__ __forceinline__ void jitter_warp(const Params& P) {
+    if (P.jitter_ns == 0) return;
+    uint32_t x = (uint32_t)globaltimer() * 2654435761u ^ ((threadIdx.x >> 5) * 40503u) ^ (blockIdx.x * 2246822519u);
+    x ^= x >> 15;
+    x *= 2246822519u;
+    x ^= x >> 13;
+    x = __shfl_sync(0xffffffffu, x, 0);
+    if ((x & 7u) == 0) __nanosleep(x % P.jitter_ns);
+    __syncwarp();
 }
 
 // ------------------------------------------------------------------ errors

@@ -382,7 +382,7 @@ template <> struct Wire<POLAR_PROTO_LL128> {
         return slot_bytes / kLL128UnitBytes;
     }
     static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long k, uint4 v, uint64_t f) {
-        jitter(P);
+        jitter_warp(P);
         __syncwarp();
         st_ll128(slot + (kLL128UnitBytes / 16) * k, v, f);
     }

@@ -79,3 +79,15 @@ def test_missing_rank_times_out(tmp_path, algo, proto):
     assert r0["status"] == "etimeout"
     assert r0["next_call"] == "etimeout"
     assert r0["seconds"] < 60
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_ll128_line_atomicity_probe(mode):
+    """The LL128 premise on this GPU (polar_probe_ll128): a reader that sees a
+    line's flag sees that line's payload, with readers spinning while writers
+    are delayed warp-uniformly (mode 1, the LL128 fault injection) or by
+    per-lane divergent busy waits (mode 2).  Per-lane NANOSLEEP before the store
+    (mode 0) is known to tear (profiles/r01_probe_ll128.jsonl) and is not used."""
+    torn, reads = L.probe_ll128(0, pairs=32, iters=20000, jitter_ns=2000, jitter_mode=mode)
+    assert reads == 32 * 20000 * 32
+    assert torn == 0
