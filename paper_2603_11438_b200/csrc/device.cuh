@@ -242,20 +242,29 @@ __device__ __forceinline__ void raise_error(const Params& P, int code) {
     __threadfence_system();
 }
 
-// Spin until *p >= v; false on timeout (error latched).
-static __device__ __noinline__ bool wait_geq(const Params& P, const uint64_t* p, uint64_t v) {
-    if (ld_acquire(p, P.sys) >= v) return true;
+// Spin until *p >= v; false on timeout (error latched).  The spin loop is out
+// of line (code size) and takes the few Params fields it needs BY VALUE: passing
+// `const Params&` to a non-inlined function takes the kernel parameter's
+// address, which makes every thread copy the whole Params block to its local
+// stack at kernel entry (measured: +2 us per two-shot call).
+static __device__ __noinline__ bool wait_geq_slow(const uint64_t* p, uint64_t v, int sys,
+                                                  unsigned long long timeout_ns, int* err) {
     const uint64_t t0 = globaltimer();
     for (uint32_t it = 1;; ++it) {
-        if (ld_acquire(p, P.sys) >= v) return true;
+        if (ld_acquire(p, sys) >= v) return true;
         if ((it & 255) == 0) {
-            if (globaltimer() - t0 > P.timeout_ns) {
-                raise_error(P, POLAR_ETIMEOUT);
+            if (globaltimer() - t0 > timeout_ns) {
+                *(volatile int*)err = POLAR_ETIMEOUT;
+                __threadfence_system();
                 return false;
             }
-            if (*(volatile int*)P.err) return false;   // someone else failed: give up too
+            if (*(volatile int*)err) return false;   // someone else failed: give up too
         }
     }
+}
+__device__ __forceinline__ bool wait_geq(const Params& P, const uint64_t* p, uint64_t v) {
+    if (ld_acquire(p, P.sys) >= v) return true;
+    return wait_geq_slow(p, v, P.sys, P.timeout_ns, P.err);
 }
 
 // Poll one LL line until both flags equal `flag`; false on timeout.
@@ -276,18 +285,35 @@ __device__ __forceinline__ bool poll_ll(const Params& P, const uint4* p, uint32_
     }
 }
 
-// Poll one LL128 line group until all four flags equal `flag`, then hand lane
-// L < 30 its pack L (lanes 30, 31 get padding).  Warp-uniform result; false on
-// timeout (error latched).
+// LL128 reader helpers: does this lane's 16 B of a line group carry `flag`
+// (only flag lanes check), and the inverse of st_ll128's shuffle (lane L < 30
+// gets pack L; lanes 30, 31 get padding).  Both warp-collective (shuffles).
+__device__ __forceinline__ bool ll128_lane_ready(const uint4& w, uint64_t flag) {
+    return (threadIdx.x & 7) != 7 || (w.z == (uint32_t)flag && w.w == (uint32_t)(flag >> 32));
+}
+__device__ __forceinline__ uint4 ll128_unpack(const uint4& w) {
+    const int lane = (int)(threadIdx.x & 31);
+    const int s0 = lane < 28 ? (lane / 7) * 8 + lane % 7 : (lane == 28 ? 7 : 23);
+    const int s1 = lane == 29 ? 31 : 15;
+    uint4 a;
+    a.x = __shfl_sync(0xffffffffu, w.x, s0);
+    a.y = __shfl_sync(0xffffffffu, w.y, s0);
+    a.z = __shfl_sync(0xffffffffu, w.z, s0);
+    a.w = __shfl_sync(0xffffffffu, w.w, s0);
+    const uint32_t b0 = __shfl_sync(0xffffffffu, w.x, s1);
+    const uint32_t b1 = __shfl_sync(0xffffffffu, w.y, s1);
+    return lane < 28 ? a : make_uint4(a.x, a.y, b0, b1);
+}
+
+// Poll one LL128 line group until all four flags equal `flag`, then unpack.
+// Warp-uniform result; false on timeout (error latched).
 __device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, uint64_t flag, uint4& out) {
-    const int lane = (int)(threadIdx.x & 31), q = lane & 7;
-    const uint32_t flo = (uint32_t)flag, fhi = (uint32_t)(flag >> 32);
+    const int lane = (int)(threadIdx.x & 31);
     uint4 w;
     uint64_t t0 = 0;
     for (uint32_t it = 0;; ++it) {
         w = ld_ll(group + lane);
-        const bool mine = q != 7 || (w.z == flo && w.w == fhi);
-        if (__all_sync(0xffffffffu, mine)) break;
+        if (__all_sync(0xffffffffu, ll128_lane_ready(w, flag))) break;
         if ((it & 1023) == 1023) {
             int bad = 0;
             if (lane == 0) {
@@ -299,16 +325,7 @@ __device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, ui
             if (__shfl_sync(0xffffffffu, bad, 0)) return false;
         }
     }
-    const int s0 = lane < 28 ? (lane / 7) * 8 + lane % 7 : (lane == 28 ? 7 : 23);
-    const int s1 = lane == 29 ? 31 : 15;
-    uint4 a;
-    a.x = __shfl_sync(0xffffffffu, w.x, s0);
-    a.y = __shfl_sync(0xffffffffu, w.y, s0);
-    a.z = __shfl_sync(0xffffffffu, w.z, s0);
-    a.w = __shfl_sync(0xffffffffu, w.w, s0);
-    const uint32_t b0 = __shfl_sync(0xffffffffu, w.x, s1);
-    const uint32_t b1 = __shfl_sync(0xffffffffu, w.y, s1);
-    out = lane < 28 ? a : make_uint4(a.x, a.y, b0, b1);
+    out = ll128_unpack(w);
     return true;
 }
 

@@ -344,10 +344,29 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
 // How packs travel through staging slots and FIFOs, per protocol.  A slot is
 // addressed by WIRE INDEX k: Simple = one 16-B pack, LL = one pack as two 16-B LL
 // lines, LL128 = one warp unit of kLL128Packs packs as a 512-B line group.
-// put/get of LL128 are warp-collective (every lane calls them; see for_packs).
+// put/get of LL128 are warp-collective (every lane calls them; see for_batch).
 //   Simple: payload only; ordering comes from a separate fence + flag.
 //   LL    : flag-in-data, flag = (u32) sequence number.
 //   LL128 : flag per 128-B line, flag = u64 sequence number.
+//
+// Latency hiding: every loop moves a BATCH of wire indices per thread
+// (Simple / LL) or per warp (LL128) per iteration, and get_batch issues all of
+// the batch's loads before it looks at any of them, so several 16-B loads per
+// thread are in flight instead of one (Little's law over peer latency).
+
+// Simple moves 4 packs per thread per iteration; LL / LL128 2 (their polls hold
+// twice the registers per pack; 4 spilled at the 128-register cap of 512-thread
+// CTAs).  bf16 (f32 partials on the wire) halves the batch in ring / tree.
+template <int PROTO> __host__ __device__ constexpr int batch_for() { return PROTO == POLAR_PROTO_SIMPLE ? 4 : 2; }
+
+// One iteration's packs.  Simple / LL: pack i[u] = i0 + u * blockDim, wire index
+// j[u] = i[u] - lo.  LL128: unit j[u] = u0 + u * nwarps (warp-uniform), pack
+// i[u] = lo + 30 j[u] + lane.  in[u]: the wire index is used (warp-uniform for
+// LL128); act[u]: this thread holds a pack of the message.
+template <int U> struct Batch {
+    unsigned long long i[U], j[U];
+    bool in[U], act[U];
+};
 
 template <int PROTO> struct Wire;
 
@@ -357,8 +376,14 @@ template <> struct Wire<POLAR_PROTO_SIMPLE> {
     static __device__ __forceinline__ void put(const Params&, uint4* slot, unsigned long long k, uint4 v, uint64_t) {
         st_plain(slot + k, v);
     }
-    static __device__ __forceinline__ bool get(const Params&, const uint4* slot, unsigned long long k, uint64_t, uint4& v) {
-        v = ld_cg(slot + k);
+    template <int U, int NW>
+    static __device__ __forceinline__ bool get_batch(const Params&, const uint4* slot, const Batch<U>& b, uint64_t,
+                                                     uint4 (&v)[U][NW]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) v[u][q] = ld_cg(slot + b.j[u] * NW + q);
         return true;
     }
 };
@@ -369,10 +394,31 @@ template <> struct Wire<POLAR_PROTO_LL> {
         jitter(P), st_ll(slot + 2 * k, v.x, v.y, (uint32_t)f);
         jitter(P), st_ll(slot + 2 * k + 1, v.z, v.w, (uint32_t)f);
     }
-    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long k, uint64_t f, uint4& v) {
-        uint4 l0, l1;
-        if (!poll_ll(P, slot + 2 * k, (uint32_t)f, l0) || !poll_ll(P, slot + 2 * k + 1, (uint32_t)f, l1)) return false;
-        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
+    template <int U, int NW>
+    static __device__ __forceinline__ bool get_batch(const Params& P, const uint4* slot, const Batch<U>& b, uint64_t f,
+                                                     uint4 (&v)[U][NW]) {
+        const uint32_t fl = (uint32_t)f;
+        uint4 l[U][NW][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) {
+                    l[u][q][0] = ld_ll(slot + 2 * (b.j[u] * NW + q));
+                    l[u][q][1] = ld_ll(slot + 2 * (b.j[u] * NW + q) + 1);
+                }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) {
+                    const uint4* p = slot + 2 * (b.j[u] * NW + q);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (l[u][q][h].y != fl || l[u][q][h].w != fl)
+                            if (!poll_ll(P, p + h, fl, l[u][q][h])) return false;
+                    v[u][q] = make_uint4(l[u][q][0].x, l[u][q][0].z, l[u][q][1].x, l[u][q][1].z);
+                }
         return true;
     }
 };
@@ -386,29 +432,62 @@ template <> struct Wire<POLAR_PROTO_LL128> {
         __syncwarp();
         st_ll128(slot + (kLL128UnitBytes / 16) * k, v, f);
     }
-    static __device__ __forceinline__ bool get(const Params& P, const uint4* slot, unsigned long long k, uint64_t f, uint4& v) {
+    template <int U, int NW>
+    static __device__ __forceinline__ bool get_batch(const Params& P, const uint4* slot, const Batch<U>& b, uint64_t f,
+                                                     uint4 (&v)[U][NW]) {
+        const unsigned lane = threadIdx.x & 31;
+        uint4 w[U][NW];
         __syncwarp();
-        return ld_ll128(P, slot + (kLL128UnitBytes / 16) * k, f, v);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) w[u][q] = ld_ll(slot + (kLL128UnitBytes / 16) * (b.j[u] * NW + q) + lane);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) {
+                    if (__all_sync(0xffffffffu, ll128_lane_ready(w[u][q], f))) {
+                        v[u][q] = ll128_unpack(w[u][q]);
+                    } else if (!ld_ll128(P, slot + (kLL128UnitBytes / 16) * (b.j[u] * NW + q), f, v[u][q])) {
+                        return false;
+                    }
+                }
+        return true;
     }
 };
 
-// Run body(i, j, act) over packs [lo, hi).  Simple / LL: one pack per thread,
-// j = i - lo (the pack's wire index relative to lo).  LL128: one unit of 30
-// packs per warp, j = the unit index relative to lo, i = lo + 30 j + lane; the
-// whole warp runs the body (warp-collective wires) and `act` is false on lanes
-// without a pack.  The body returns false to stop (timeout); so does for_packs.
-template <int PROTO, class Body>
-__device__ __forceinline__ bool for_packs(unsigned long long lo, unsigned long long hi, Body&& body) {
+// Run body(batch) over packs [lo, hi) in batches of U (see Batch).  The body
+// returns false to stop (timeout); so does for_batch.  For LL128 the whole warp
+// runs every iteration (warp-collective wires).
+template <int PROTO, int U, class Body>
+__device__ __forceinline__ bool for_batch(unsigned long long lo, unsigned long long hi, Body&& body) {
+    Batch<U> b;
     if constexpr (PROTO == POLAR_PROTO_LL128) {
         const unsigned lane = threadIdx.x & 31;
         const unsigned long long nw = blockDim.x >> 5;
-        for (unsigned long long u = threadIdx.x >> 5; lo + u * kLL128Packs < hi; u += nw) {
-            const unsigned long long i = lo + u * kLL128Packs + lane;
-            if (!body(i, u, lane < (unsigned)kLL128Packs && i < hi)) return false;
+        for (unsigned long long u0 = threadIdx.x >> 5; lo + u0 * kLL128Packs < hi; u0 += U * nw) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                b.j[u] = u0 + u * nw;
+                b.in[u] = lo + b.j[u] * kLL128Packs < hi;
+                b.i[u] = lo + b.j[u] * kLL128Packs + lane;
+                b.act[u] = b.in[u] && lane < (unsigned)kLL128Packs && b.i[u] < hi;
+            }
+            if (!body(b)) return false;
         }
     } else {
-        for (unsigned long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
-            if (!body(i, i - lo, true)) return false;
+        const unsigned long long B = blockDim.x;
+        for (unsigned long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * B) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                b.i[u] = i0 + u * B;
+                b.j[u] = b.i[u] - lo;
+                b.in[u] = b.act[u] = b.i[u] < hi;
+            }
+            if (!body(b)) return false;
+        }
     }
     return true;
 }
@@ -423,6 +502,13 @@ __device__ __forceinline__ Geo make_geo_for(unsigned long long NP, unsigned long
 
 __device__ __forceinline__ uint4 zero4() { return make_uint4(0, 0, 0, 0); }
 
+// own packs of a batch (issued together; zeros where the thread holds no pack)
+template <int ES, int U>
+__device__ __forceinline__ void load_batch(const Params& P, const char* base, const Batch<U>& b, uint4 (&v)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = b.act[u] ? load_pack<ES>(P, base, b.i[u]) : zero4();
+}
+
 // Two-shot LL / LL128: push-based.  RS: rank r writes its part of owner j's
 // shard into j's RS staging slot r; owner polls, reduces in rank order, writes
 // its own buffer and pushes the result into every rank's AG slot; every rank
@@ -435,9 +521,18 @@ __device__ __forceinline__ uint4* ts_stage(const Params& P, int owner, int ag, i
                                     ((size_t)(par * kMaxRanks + slot)) * 2 * P.tsll_chunk);
 }
 
+// shift a batch's wire indices by a staging region offset (in wire units)
+template <int U> __device__ __forceinline__ Batch<U> shifted(const Batch<U>& b, unsigned long long ob) {
+    Batch<U> s = b;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s.j[u] += ob;
+    return s;
+}
+
 template <int DT, int OP, int PROTO>
 __device__ void twoshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
+    constexpr int U = batch_for<PROTO>();
     using W = Wire<PROTO>;
     const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
@@ -456,30 +551,45 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
             geo_slice(g, NP, k, j, w.c, lo, hi, off);
             uint4* dst = ts_stage<PROTO>(P, j, 0, par, w.r);
             const unsigned long long ob = off / W::kPacks;
-            for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
-                W::put(P, dst, ob + jj, act ? load_pack<ES>(P, mine, i) : zero4(), e);
+            for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+                uint4 v[U];
+                load_batch<ES>(P, mine, b, v);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b.in[u]) W::put(P, dst, ob + b.j[u], v[u], e);
                 return true;
             });
         }
         // reduce my part in rank order, keep it and push it to every rank
         geo_slice(g, NP, k, w.r, w.c, lo, hi, off);
         const unsigned long long ob = off / W::kPacks;
-        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
-            Acc<DT> acc;
+        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+            const Batch<U> sb = shifted(b, ob);
+            uint4 own[U];
+            load_batch<ES>(P, mine, b, own);
+            Acc<DT> acc[U];
             for (int p = 0; p < n; ++p) {
-                uint4 v = zero4();
+                uint4 v[U][1];
                 if (p == w.r) {
-                    if (act) v = load_pack<ES>(P, mine, i);
-                } else if (!W::get(P, ts_stage<PROTO>(P, w.r, 0, par, p), ob + jj, e, v)) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u][0] = own[u];
+                } else if (!W::template get_batch<U, 1>(P, ts_stage<PROTO>(P, w.r, 0, par, p), sb, e, v)) {
                     return false;
                 }
-                if (p == 0) acc_init<DT>(acc, v);
-                else acc_add<DT, OP>(acc, v);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (p == 0) acc_init<DT>(acc[u], v[u][0]);
+                    else acc_add<DT, OP>(acc[u], v[u][0]);
+                }
             }
-            const uint4 out = acc_fin<DT>(acc);
-            if (act) store_pack<ES>(P, mine, i, out);
-            for (int p = 0; p < n; ++p)
-                if (p != w.r) W::put(P, ts_stage<PROTO>(P, p, 1, par, w.r), ob + jj, out, e);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!b.in[u]) continue;
+                const uint4 out = acc_fin<DT>(acc[u]);
+                if (b.act[u]) store_pack<ES>(P, mine, b.i[u], out);
+                for (int p = 0; p < n; ++p)
+                    if (p != w.r) W::put(P, ts_stage<PROTO>(P, p, 1, par, w.r), sb.j[u], out, e);
+            }
             return true;
         });
         // AG receive: results of every other owner
@@ -488,10 +598,12 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
             geo_slice(g, NP, k, j, w.c, lo, hi, off);
             const uint4* src = ts_stage<PROTO>(P, w.r, 1, par, j);
             const unsigned long long obj = off / W::kPacks;
-            ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long jj, bool act) {
-                uint4 v;
-                if (!W::get(P, src, obj + jj, e, v)) return false;
-                if (act) store_pack<ES>(P, mine, i, v);
+            ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+                uint4 v[U][1];
+                if (!W::template get_batch<U, 1>(P, src, shifted(b, obj), e, v)) return false;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b.act[u]) store_pack<ES>(P, mine, b.i[u], v[u][0]);
                 return true;
             });
         }
@@ -517,6 +629,7 @@ __device__ __forceinline__ uint4* osll_slot(const Params& P, int owner, int par,
 template <int DT, int OP>
 __device__ void oneshot_simple(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
+    constexpr int U = batch_for<POLAR_PROTO_SIMPLE>();
     const int n = w.n, tid = w.tid;
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e0 = st->epoch;
@@ -528,12 +641,17 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
         const int par = (int)(e & 1);
         unsigned long long lo, hi, off;
         geo_slice(g, NP, k, 0, w.c, lo, hi, off);
-        for (unsigned long long i = lo + tid; i < hi; i += blockDim.x) {
-            const uint4 v = load_pack<ES>(P, mine, i);
+        for_batch<POLAR_PROTO_SIMPLE, U>(lo, hi, [&](const Batch<U>& b) {
+            uint4 v[U];
+            load_batch<ES>(P, mine, b, v);
 #pragma unroll
-            for (int p = 0; p < kMaxRanks; ++p)
-                if (p < n && p != w.r) st_plain(os_slot(P, p, par, w.r) + off + (i - lo), v);
-        }
+            for (int u = 0; u < U; ++u)
+                if (b.in[u])
+#pragma unroll
+                    for (int p = 0; p < kMaxRanks; ++p)
+                        if (p < n && p != w.r) st_plain(os_slot(P, p, par, w.r) + off + b.j[u], v[u]);
+            return true;
+        });
         __syncthreads();
         if (tid < n && tid != w.r) {
             fence_acq_rel(P.sys);
@@ -562,6 +680,7 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
 template <int DT, int OP, int PROTO>
 __device__ void oneshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
+    constexpr int U = batch_for<PROTO>();
     using W = Wire<PROTO>;
     const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
@@ -576,25 +695,38 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
         unsigned long long lo, hi, off;
         geo_slice(g, NP, k, 0, w.c, lo, hi, off);
         const unsigned long long ob = off / W::kPacks;
-        for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
-            const uint4 v = act ? load_pack<ES>(P, mine, i) : zero4();
-            for (int p = 0; p < n; ++p)
-                if (p != w.r) W::put(P, osll_slot<PROTO>(P, p, par, w.r), ob + j, v, e);
+        for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+            uint4 v[U];
+            load_batch<ES>(P, mine, b, v);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b.in[u])
+                    for (int p = 0; p < n; ++p)
+                        if (p != w.r) W::put(P, osll_slot<PROTO>(P, p, par, w.r), ob + b.j[u], v[u], e);
             return true;
         });
-        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
-            Acc<DT> acc;
+        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+            const Batch<U> sb = shifted(b, ob);
+            uint4 own[U];
+            load_batch<ES>(P, mine, b, own);
+            Acc<DT> acc[U];
             for (int p = 0; p < n; ++p) {
-                uint4 v = zero4();
+                uint4 v[U][1];
                 if (p == w.r) {
-                    if (act) v = load_pack<ES>(P, mine, i);
-                } else if (!W::get(P, osll_slot<PROTO>(P, w.r, par, p), ob + j, e, v)) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u][0] = own[u];
+                } else if (!W::template get_batch<U, 1>(P, osll_slot<PROTO>(P, w.r, par, p), sb, e, v)) {
                     return false;
                 }
-                if (p == 0) acc_init<DT>(acc, v);
-                else acc_add<DT, OP>(acc, v);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (p == 0) acc_init<DT>(acc[u], v[u][0]);
+                    else acc_add<DT, OP>(acc[u], v[u][0]);
+                }
             }
-            if (act) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b.act[u]) store_pack<ES>(P, mine, b.i[u], acc_fin<DT>(acc[u]));
             return true;
         });
         if (!__syncthreads_and(ok)) return;   // parity reuse safety
@@ -635,6 +767,7 @@ template <int DT, int OP, int PROTO>
 __device__ void ring(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int AW = AccWords<DT>::N;
+    constexpr int U = batch_for<PROTO>() / AW > 0 ? batch_for<PROTO>() / AW : 1;
     using W = Wire<PROTO>;
     const int n = w.n, tid = w.tid, r = w.r, c = w.c;
     const int next = (r + 1) % n, prev = (r + n - 1) % n;
@@ -673,31 +806,46 @@ __device__ void ring(const Params& P, const Who& w) {
             const uint4* src = ring_slot<PROTO>(P, r, c, recvd);
             uint4* dst = ring_slot<PROTO>(P, next, c, sent);
             const uint64_t fin = recvd + 1, fout = sent + 1;
-            ok = for_packs<PROTO>(ks, ke, [&](unsigned long long i, unsigned long long j, bool act) {
+            ok = for_batch<PROTO, U>(ks, ke, [&](const Batch<U>& b) {
+                uint4 own[U];
+                if (s < n) load_batch<ES>(P, mine, b, own);
                 if (s == 0) {
-                    Acc<DT> acc;
-                    acc_init<DT>(acc, act ? load_pack<ES>(P, mine, i) : zero4());
 #pragma unroll
-                    for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
+                    for (int u = 0; u < U; ++u) {
+                        if (!b.in[u]) continue;
+                        Acc<DT> acc;
+                        acc_init<DT>(acc, own[u]);
+#pragma unroll
+                        for (int q = 0; q < AW; ++q) W::put(P, dst, b.j[u] * AW + q, acc.w[q], fout);
+                    }
                 } else if (s < n) {
-                    Acc<DT> acc;
+                    uint4 in[U][AW];
+                    if (!W::template get_batch<U, AW>(P, src, b, fin, in)) return false;
 #pragma unroll
-                    for (int q = 0; q < AW; ++q)
-                        if (!W::get(P, src, j * AW + q, fin, acc.w[q])) return false;
-                    if (act) acc_add<DT, OP>(acc, load_pack<ES>(P, mine, i));
-                    if (s < n - 1) {
+                    for (int u = 0; u < U; ++u) {
+                        if (!b.in[u]) continue;
+                        Acc<DT> acc;
 #pragma unroll
-                        for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
-                    } else {
-                        const uint4 out = acc_fin<DT>(acc);
-                        if (act) store_pack<ES>(P, mine, i, out);
-                        W::put(P, dst, j, out, fout);
+                        for (int q = 0; q < AW; ++q) acc.w[q] = in[u][q];
+                        if (b.act[u]) acc_add<DT, OP>(acc, own[u]);
+                        if (s < n - 1) {
+#pragma unroll
+                            for (int q = 0; q < AW; ++q) W::put(P, dst, b.j[u] * AW + q, acc.w[q], fout);
+                        } else {
+                            const uint4 out = acc_fin<DT>(acc);
+                            if (b.act[u]) store_pack<ES>(P, mine, b.i[u], out);
+                            W::put(P, dst, b.j[u], out, fout);
+                        }
                     }
                 } else {
-                    uint4 v;
-                    if (!W::get(P, src, j, fin, v)) return false;
-                    if (act) store_pack<ES>(P, mine, i, v);
-                    if (do_send) W::put(P, dst, j, v, fout);
+                    uint4 v[U][1];
+                    if (!W::template get_batch<U, 1>(P, src, b, fin, v)) return false;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (!b.in[u]) continue;
+                        if (b.act[u]) store_pack<ES>(P, mine, b.i[u], v[u][0]);
+                        if (do_send) W::put(P, dst, b.j[u], v[u][0], fout);
+                    }
                 }
                 return true;
             });
@@ -747,6 +895,7 @@ template <int DT, int OP, int PROTO>
 __device__ void tree(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int AW = AccWords<DT>::N;
+    constexpr int U = batch_for<PROTO>() / AW > 0 ? batch_for<PROTO>() / AW : 1;
     using W = Wire<PROTO>;
     const int n = w.n, tid = w.tid, r = w.r, c = w.c;
     const int pos = ((r - c) % n + n) % n;
@@ -783,22 +932,33 @@ __device__ void tree(const Params& P, const Who& w) {
         if (!__syncthreads_and(ok)) return;
         uint4* dst = root ? nullptr : tree_up_slot<PROTO>(P, parent, c, my_child_idx, usent);
         const uint64_t fout = usent + 1;
-        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
-            Acc<DT> acc;
-            acc_init<DT>(acc, act ? load_pack<ES>(P, mine, i) : zero4());
+        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+            uint4 own[U];
+            load_batch<ES>(P, mine, b, own);
+            Acc<DT> acc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc_init<DT>(acc[u], own[u]);
             for (int k = 0; k < nchild; ++k) {
-                const uint4* src = tree_up_slot<PROTO>(P, r, c, k, urecv[k]);
-                Acc<DT> b;
+                uint4 in[U][AW];
+                if (!W::template get_batch<U, AW>(P, tree_up_slot<PROTO>(P, r, c, k, urecv[k]), b, urecv[k] + 1, in))
+                    return false;
 #pragma unroll
-                for (int q = 0; q < AW; ++q)
-                    if (!W::get(P, src, j * AW + q, urecv[k] + 1, b.w[q])) return false;
-                acc_merge<DT, OP>(acc, b);
+                for (int u = 0; u < U; ++u) {
+                    Acc<DT> ch;
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) ch.w[q] = in[u][q];
+                    if (b.in[u]) acc_merge<DT, OP>(acc[u], ch);
+                }
             }
-            if (root) {
-                if (act) store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
-            } else {
 #pragma unroll
-                for (int q = 0; q < AW; ++q) W::put(P, dst, j * AW + q, acc.w[q], fout);
+            for (int u = 0; u < U; ++u) {
+                if (!b.in[u]) continue;
+                if (root) {
+                    if (b.act[u]) store_pack<ES>(P, mine, b.i[u], acc_fin<DT>(acc[u]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) W::put(P, dst, b.j[u] * AW + q, acc[u].w[q], fout);
+                }
             }
             return true;
         });
@@ -826,15 +986,23 @@ __device__ void tree(const Params& P, const Who& w) {
         if (!__syncthreads_and(ok)) return;
         const uint4* src = root ? nullptr : tree_dn_slot<PROTO>(P, r, c, drecv);
         const uint64_t fin = drecv + 1, fout = dsent + 1;
-        ok = for_packs<PROTO>(lo, hi, [&](unsigned long long i, unsigned long long j, bool act) {
-            uint4 v = zero4();
+        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
+            uint4 v[U][1];
             if (root) {
-                if (act) v = load_pack<ES>(P, mine, i);
+                uint4 own[U];
+                load_batch<ES>(P, mine, b, own);
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u][0] = own[u];
             } else {
-                if (!W::get(P, src, j, fin, v)) return false;
-                if (act) store_pack<ES>(P, mine, i, v);
+                if (!W::template get_batch<U, 1>(P, src, b, fin, v)) return false;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b.act[u]) store_pack<ES>(P, mine, b.i[u], v[u][0]);
             }
-            for (int k = 0; k < nchild; ++k) W::put(P, tree_dn_slot<PROTO>(P, child[k], c, dsent), j, v, fout);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b.in[u])
+                    for (int k = 0; k < nchild; ++k) W::put(P, tree_dn_slot<PROTO>(P, child[k], c, dsent), b.j[u], v[u][0], fout);
             return true;
         });
         if (!__syncthreads_and(ok)) return;

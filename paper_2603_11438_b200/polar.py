@@ -136,8 +136,7 @@ _sigs = {
                                           C.POINTER(C.c_uint32)]),
     "polar_status_string": (C.c_char_p, [C.c_int]),
     "polar_version": (C.c_char_p, []),
-    "polar_probe_ll128": (C.c_int, [C.c_int, C.c_int, C.c_ulonglong, C.c_uint, C.c_int, C.POINTER(C.c_ulonglong),
-                                    C.POINTER(C.c_ulonglong)]),
+
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)
@@ -438,8 +437,12 @@ class Comm:
 
 def probe_ll128(device=0, pairs=64, iters=20000, jitter_ns=0, jitter_mode=0):
     """(torn lanes, lanes read) of the LL128 hardware probe (polar.h)."""
+    fn = lib.polar_probe_ll128   # diagnostic: bound on first use
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int, C.c_int, C.c_ulonglong, C.c_uint, C.c_int, C.POINTER(C.c_ulonglong),
+                   C.POINTER(C.c_ulonglong)]
     torn, reads = C.c_ulonglong(0), C.c_ulonglong(0)
-    _check(lib.polar_probe_ll128(int(device), int(pairs), int(iters), int(jitter_ns), int(jitter_mode),
+    _check(fn(int(device), int(pairs), int(iters), int(jitter_ns), int(jitter_mode),
                                  C.byref(torn), C.byref(reads)),
            "polar_probe_ll128")
     return torn.value, reads.value
