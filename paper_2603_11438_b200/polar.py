@@ -143,7 +143,7 @@ for _name, (_res, _args) in _sigs.items():
     _f.restype = _res
     _f.argtypes = _args
 
-EXPORTED = tuple(_sigs)
+EXPORTED = tuple(_sigs) + ("polar_probe_ll128",)   # + diagnostics bound on first use
 
 
 def _check(st, what):
