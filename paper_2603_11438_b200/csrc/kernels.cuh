@@ -97,7 +97,13 @@ struct TwoShotGeo {
     unsigned long long s0, s1, nbig, bigend, nchunks, nfull, wbase;
     unsigned long long* work;
 };
-constexpr unsigned long long kTsBig = 2048, kTsSmall = 256;   // packs (32 KiB / 4 KiB per buffer)
+#ifndef POLAR_TS_BIG
+#define POLAR_TS_BIG 2048
+#endif
+#ifndef POLAR_TS_SMALL
+#define POLAR_TS_SMALL 512
+#endif
+constexpr unsigned long long kTsBig = POLAR_TS_BIG, kTsSmall = POLAR_TS_SMALL;   // packs (32 KiB / 8 KiB per buffer)
 
 template <int DT, int OP, int N>
 __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, const TwoShotGeo& g) {

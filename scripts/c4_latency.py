@@ -32,7 +32,8 @@ def ev_time(fn, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8)
-    ap.add_argument("--algos", default="oneshot:ll,twoshot:ll,tree:ll,ring:ll,oneshot:simple,twoshot:simple")
+    ap.add_argument("--algos", default="oneshot:ll,oneshot:ll128,twoshot:ll,twoshot:ll128,tree:ll,tree:ll128,ring:ll,"
+                                       "ring:ll128,oneshot:simple,twoshot:simple")
     ap.add_argument("--nch", default="1,2,3,4")
     ap.add_argument("--iters", type=int, default=200)
     a = ap.parse_args()

@@ -5,7 +5,7 @@ python scripts/report_configs.py [--configs 1,2,3,5] > gpurun_out/configs.jsonl
       parity (bit-exact vs oracle, whole vectors), decision == oracle mapping, t, busBW
   C2  8-rank fp32 sum, 4-128 MiB: default policy vs every forced (algo, proto) at its best
       channel count, vs the best single global choice (E10), vs bad_channels (E11)
-  C3  bf16 sum, 4 KiB-1 GiB at 2/4/8 ranks: forced {oneshot, twoshot, ring, tree} x {LL, Simple}
+  C3  bf16 sum, 4 KiB-1 GiB at 2/4/8 ranks: forced {oneshot, twoshot, ring, tree} x {LL, LL128, Simple}
       (16 channels) and policy-selected; sampled parity at every size
   C5  400,000 decisions (p50/p99/batched), swap stress (4 invokers, 1000 swaps)
 C4 is scripts/c4_latency.py.  Peers are local HBM (virtual ranks), so these are
@@ -29,8 +29,7 @@ from oracle import policy as opol  # noqa: E402
 from paper_2603_11438_b200 import polar as L  # noqa: E402
 from tests.gpu_common import to_device, to_host  # noqa: E402
 
-ALGOS = [("oneshot", "ll"), ("oneshot", "simple"), ("twoshot", "ll"), ("twoshot", "simple"),
-         ("ring", "ll"), ("ring", "simple"), ("tree", "ll"), ("tree", "simple")]
+ALGOS = [(a, p) for a in ("oneshot", "twoshot", "ring", "tree") for p in ("ll", "ll128", "simple")]
 
 
 def emit(d):
@@ -120,6 +119,13 @@ def c2():
                     best = (round(bw, 1), nch)
             forced[f"{algo}/{proto}"] = best
         rec["forced_best"] = forced
+        # the paper's case-study policy as a table (Ring/LL128 4-32 MiB, Ring/Simple 64-192 MiB)
+        L.set_policy(load_rows("nvlink_ring_mid_v2.json"))
+        it, _ = iters_for(lambda: comm.allreduce(v), 0.05)
+        tp = ev_time(lambda: comm.allreduce(v), it)
+        d = comm.last_decision()
+        rec["nvlink_ring_mid_v2"] = {"decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
+                                     "busbw_gbs": round(busbw(size, n, tp), 1)}
         # bad_channels: a policy forcing 1 channel, everything else deferred
         L.set_policy([(0, 0, 2**64 - 1, L.UNSET, L.UNSET, 1)])
         it, _ = iters_for(lambda: comm.allreduce(v), 0.05)
