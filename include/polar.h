@@ -196,9 +196,12 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
 polar_status polar_bootstrap_check(int nranks, int rank, polar_allgather_fn ag, void* user);
 
 /* Virtual comm: nranks logical ranks hosted by THIS process on ONE device; one
- * kernel launch runs every rank's CTAs (grid = nranks x nchannels, a cooperative
- * launch so that cross-rank waits cannot deadlock).  Same kernels, same
- * protocols; peers are local HBM instead of NVLink. */
+ * kernel launch runs every rank's CTAs (grid = nranks x nchannels, clamped to
+ * the device's co-resident CTA count so that cross-rank waits cannot deadlock
+ * on an otherwise idle GPU; plain launch + programmatic dependent launch like
+ * real comms, POLAR_VIRTUAL_COOP=1 forces a cooperative launch).  Same kernels,
+ * same protocols; peers are local HBM instead of NVLink (DESIGN.md "Virtual
+ * ranks").  Every cross-rank wait is bounded (POLAR_TIMEOUT_MS). */
 polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device);
 
 /* Collective for real comms: synchronises the device, host-barriers through the

@@ -1,6 +1,6 @@
 """polar operator CLI (host side; SPEC.md cli module L560-592 analog).
 
-    python -m paper_2603_11438_b200.cli validate policies/b200_virtual8.json
+    python -m paper_2603_11438_b200.cli validate policies/b200_virtual.json
     python -m paper_2603_11438_b200.cli explain  policies/listing1_size_aware.json --nranks 8
     python -m paper_2603_11438_b200.cli decide   policies/c1_fixed_threshold.json --nranks 2 --bytes 65536
     python -m paper_2603_11438_b200.cli bench-decide [--calls 400000]

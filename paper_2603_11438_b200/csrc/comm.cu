@@ -666,9 +666,15 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
     c->device = cuda_device;
     c->is_virtual = true;
     {
-        // POLAR_VIRTUAL_COOP=0: plain launch (diagnostic; co-residency then relies on an idle GPU)
+        // Plain launch + PDL by default, like real comms: the grid
+        // is clamped to the co-resident bound, so every CTA becomes resident on an
+        // otherwise idle GPU; the next call's CTAs are scheduled as this call's
+        // drain (measured ~2 us per call less than a cooperative launch, whose
+        // grid must wait for the whole previous grid to leave).  A foreign kernel
+        // holding SMs can only delay residency into a bounded wait (ETIMEOUT),
+        // not hang.  POLAR_VIRTUAL_COOP=1 forces cooperative launches.
         const char* ev = std::getenv("POLAR_VIRTUAL_COOP");
-        c->coop = !(ev && ev[0] == '0');
+        c->coop = ev && ev[0] == '1';
     }
     c->L = make_layout(false);
     DeviceGuard dg(cuda_device);

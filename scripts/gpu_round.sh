@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU session: parity tests, smoke, bench, ncu launch list + one full capture
-# usage: bash scripts/gpu_round.sh [tag] [what...]   what in {test,smoke,bench,ncu,sweep}
+# usage: bash scripts/gpu_round.sh [tag] [what...]   what in {test,smoke,bench,ncu,configs,c4,tune,sweep}
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 TAG=${1:-r01}; shift
 WHAT=${@:-test smoke bench ncu}
@@ -30,6 +30,9 @@ for w in $WHAT; do
       echo "configs rc=$?"; tail -3 gpurun_out/configs_$TAG.jsonl | cut -c1-300 ;;
     c4)
       timeout 900 python scripts/c4_latency.py > gpurun_out/c4_$TAG.jsonl 2>&1; echo "c4 rc=$?" ;;
+    tune)
+      timeout 1800 python scripts/tune_policy.py --n 2,4,8 > gpurun_out/tune_$TAG.jsonl 2> gpurun_out/tune_$TAG.err
+      echo "tune rc=$?"; grep table gpurun_out/tune_$TAG.jsonl | cut -c1-300 ;;
     sweep)
       timeout 900 python scripts/sweep.py --n 8 --dtype f32 > gpurun_out/sweep_f32_$TAG.jsonl 2>&1
       echo "sweep rc=$?" ;;

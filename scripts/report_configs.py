@@ -253,11 +253,11 @@ def c5():
     ctxs = [(nr, 1 << k) for k in range(3, 31) for nr in (2, 4, 8)]
     s = L.bench_decide(ctxs, nwarm=10_000, ncalls=400_000)
     emit({"config": "C5", "kind": "decide_noop", **{k: round(v, 2) if isinstance(v, float) else v for k, v in s.items()}})
-    L.set_policy(load_rows("b200_virtual8.json"))
+    L.set_policy(load_rows("b200_virtual.json"))
     s = L.bench_decide(ctxs, nwarm=10_000, ncalls=400_000)
     emit({"config": "C5", "kind": "decide_tuned_table", **{k: round(v, 2) if isinstance(v, float) else v for k, v in s.items()}})
     a = [(0, 0, 32768, L.TREE, L.SIMPLE, 4), (0, 0, 2**64 - 1, L.RING, L.SIMPLE, 4)]
-    b = load_rows("b200_virtual8.json")
+    b = load_rows("b200_virtual.json")
     sw = L.bench_swap(a, b, nthreads=4, calls_per_thread=100_000, nswaps=1000)
     emit({"config": "C5", "kind": "swap_stress", **{k: round(v, 1) if isinstance(v, float) else v for k, v in sw.items()}})
     L.set_policy([])

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_validate_and_reject(capsys, tmp_path):
-    assert cli.main(["validate", os.path.join(ROOT, "policies", "b200_virtual8.json")]) == 0
+    assert cli.main(["validate", os.path.join(ROOT, "policies", "b200_virtual.json")]) == 0
     assert cli.main(["validate", os.path.join(ROOT, "policies", "nvlink_ring_mid_v2.json")]) == 0
     nvls = tmp_path / "nvls.json"
     nvls.write_text(json.dumps({"name": "nvls", "rows": [[0, 0, 1 << 30, 2, 2, 0]]}))
