@@ -363,7 +363,15 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
 // Simple moves 4 packs per thread per iteration; LL / LL128 2 (their polls hold
 // twice the registers per pack; 4 spilled at the 128-register cap of 512-thread
 // CTAs).  bf16 (f32 partials on the wire) halves the batch in ring / tree.
-template <int PROTO> __host__ __device__ constexpr int batch_for() { return PROTO == POLAR_PROTO_SIMPLE ? 4 : 2; }
+#ifndef POLAR_BATCH_SIMPLE
+#define POLAR_BATCH_SIMPLE 4
+#endif
+#ifndef POLAR_BATCH_LL
+#define POLAR_BATCH_LL 2
+#endif
+template <int PROTO> __host__ __device__ constexpr int batch_for() {
+    return PROTO == POLAR_PROTO_SIMPLE ? POLAR_BATCH_SIMPLE : POLAR_BATCH_LL;
+}
 
 // One iteration's packs.  Simple / LL: pack i[u] = i0 + u * blockDim, wire index
 // j[u] = i[u] - lo.  LL128: unit j[u] = u0 + u * nwarps (warp-uniform), pack

@@ -65,7 +65,10 @@ struct Layout {
     size_t bounce_off, bounce_bytes;  // two-shot bounce for unregistered buffers (real comms)
     size_t total;
 };
-constexpr int kSteps = 4;  // FIFO depth (slots) per connection
+#ifndef POLAR_FIFO_STEPS
+#define POLAR_FIFO_STEPS 4
+#endif
+constexpr int kSteps = POLAR_FIFO_STEPS;  // FIFO depth (slots) per connection
 
 Layout make_layout(bool with_bounce);
 
