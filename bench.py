@@ -215,6 +215,12 @@ def run_polar(args):
 
     ws, rank, local = env_dist()
     real = ws > 1
+    # test hook (tests/test_gpu_bench.py): every rank on GPU 0, so the N>1 path
+    # (one process per rank, CUDA-IPC peers, max over ranks) runs on a 1-GPU box;
+    # NCCL refuses two ranks on one GPU, so its baseline is skipped then
+    shared = os.environ.get("POLAR_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     pg = None
     if real:
@@ -345,7 +351,7 @@ def run_polar(args):
            "ms_per_step": round(t_e2e * 1e3, 3)}
 
     nccl = None
-    if real:
+    if real and not shared:
         nccl = time_nccl(args, bufs[0], count, n, stream)
 
     if rank == 0:
@@ -355,7 +361,8 @@ def run_polar(args):
             "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": round(value / PAPER_8GPU_128MIB_DEFAULT, 4) if (real and n == 8) else None,
-            "dtype": "f32", "data": "synthetic", "config": workload_config(n, real),
+            "dtype": "f32", "data": "synthetic",
+            "config": dict(workload_config(n, real), **({"shared_gpu_test": True} if shared else {})),
             "decision": {"algo": L.ALGO_NAMES[decision.algo], "proto": L.PROTO_NAMES[decision.proto],
                          "nchannels": decision.nchannels, "generation": decision.generation,
                          "launched_channels": launched_nch},

@@ -1,0 +1,50 @@
+"""The bench contract end to end on the GPU box: the N=1 line and the N>1
+torchrun path (one process per rank, CUDA-IPC peers, device timing max over
+ranks) — the latter with every rank on GPU 0 (POLAR_BENCH_SHARE_GPU=1; NCCL's
+baseline is skipped because NCCL refuses two ranks on one GPU)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+        "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _line(out):
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_torchrun_two_ranks_shared_gpu():
+    env = dict(os.environ, POLAR_BENCH_SHARE_GPU="1", POLAR_TIMEOUT_MS="20000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--steps", "5", "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    d = _line(r.stdout)
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["n_gpus"] == 2 and d["config"]["nranks"] == 2 and d["config"]["shared_gpu_test"]
+    assert d["value"] > 0 and d["gpu_launches"] == 5
+    assert d["decision"]["algo"] == "twoshot"
+    assert d["e2e"]["h2d_bytes_per_step"] == d["config"]["bytes_per_rank"]
