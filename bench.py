@@ -350,6 +350,21 @@ def run_polar(args):
            "h2d_bytes_per_step": len(bufs) * S_BYTES, "d2h_bytes_per_step": len(bufs) * S_BYTES,
            "ms_per_step": round(t_e2e * 1e3, 3)}
 
+    # p2p probe: the measured peer-path roofline on the same buffers
+    # (after the timed regions: the probe overwrites the peer buffers)
+    probe = comm.p2p_probe(bufs, iters=3)
+    if real:
+        loc = probe[0]
+        vals = [max_over_ranks(-loc["load_gbs"]), max_over_ranks(-loc["store_gbs"]), max_over_ranks(loc["pingpong_us"])]
+        probe_out = {"load_gbs_min_over_ranks": round(-vals[0], 1), "store_gbs_min_over_ranks": round(-vals[1], 1),
+                     "pingpong_us_max_over_ranks": round(vals[2], 2),
+                     "what": "each rank reads / writes peer (r+1)%n's buffer through the peer mapping, all at once"}
+    else:
+        probe_out = {"load_gbs_sum": round(sum(p["load_gbs"] for p in probe), 1),
+                     "store_gbs_sum": round(sum(p["store_gbs"] for p in probe), 1),
+                     "pingpong_us_max": round(max(p["pingpong_us"] for p in probe), 2),
+                     "what": "virtual ranks: every peer is local HBM; sums over the 8 concurrent ranks"}
+
     nccl = None
     if real and not shared:
         nccl = time_nccl(args, bufs[0], count, n, stream)
@@ -368,8 +383,12 @@ def run_polar(args):
                          "launched_channels": launched_nch},
             "algbw_gbs": round(S_BYTES / t_step / 1e9, 2),
             "nvlink_frac": round(value / 900.0, 4) if real else None,
+            "nvlink_frac_of_probe": (round(value / min(probe_out["load_gbs_min_over_ranks"],
+                                                       probe_out["store_gbs_min_over_ranks"]), 4)
+                                     if real and not shared else None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(), "c2_sweep": sweep, "decision_cost_ns": decision_cost(L),
+            "p2p_probe": probe_out,
         }
         if nccl:
             out["nccl_default"] = nccl

@@ -377,6 +377,27 @@ const char* polar_status_string(polar_status s);
 polar_status polar_probe_ll128(int cuda_device, int pairs, unsigned long long iters, unsigned jitter_ns,
                                int jitter_mode, unsigned long long* torn_lanes, unsigned long long* lane_reads);
 
+/* p2p probe (§8(d) "measure it with p2p_probe, no number
+ * is assumed"): the empirical peer-path roofline.  COLLECTIVE over the comm.
+ * bufs: nlocal device pointers to symmetric buffers of >= bytes (polar_mem_alloc
+ * on real comms, any 16-B aligned buffers on virtual comms); bytes a multiple
+ * of 16.  Every rank r, all at once, (1) reads the buffer of peer (r + 1) mod n
+ * `iters` times with 16-B loads through the peer mapping (NVLink/NVSwitch on a
+ * real node, local HBM for virtual ranks), (2) overwrites that peer buffer
+ * `iters` times with a known pattern (pack i = {i, hi32(i) ^ 0x9E3779B9, r, ~i}),
+ * (3) bounces a flag `iters` times with rank r ^ 1.  Times are device
+ * timestamps between an entry and an exit barrier.  out[nlocal]: per local
+ * rank, load / store GB/s (bytes * iters / duration), flag round trip in us (0
+ * for an unpaired last rank), and the XOR of the peer's 16-B packs as read
+ * (each pack folded to 64 bits as (w0 ^ w2) << 32 | (w1 ^ w3)).  The peer
+ * buffer holds the store pattern afterwards.  Synchronous.  EINVAL for bad
+ * arguments or an unregistered buffer on a real comm. */
+typedef struct {
+    double load_gbs, store_gbs, pingpong_us;
+    unsigned long long load_xor;
+} polar_p2p_result;
+polar_status polar_p2p_probe(polar_comm_t comm, void* const* bufs, size_t bytes, int iters, polar_p2p_result* out);
+
 const char* polar_version(void);
 
 #ifdef __cplusplus

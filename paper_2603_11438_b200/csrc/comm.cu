@@ -19,6 +19,7 @@
 
 #include "device.cuh"
 #include "dispatch.h"
+#include "p2p_probe.cuh"
 #include "polar.h"
 #include "polar_internal.h"
 
@@ -126,6 +127,7 @@ struct polar_comm_s {
     // polar_allreduce_host chunk pipeline (created on first use)
     cudaStream_t hs_in = nullptr, hs_out = nullptr;
     cudaEvent_t he_start = nullptr, he_in = nullptr, he_red = nullptr, he_out = nullptr;
+    unsigned long long probe_epoch = 0;  // p2p probe calls (same count on every rank)
     std::mutex mu;
 };
 
@@ -989,6 +991,80 @@ polar_status polar_adaptive_get_state(polar_comm_t comm, polar_adaptive_state* o
     out->samples = comm->ad.samples;
     out->last_mean_ns = comm->ad.last_mean;
     return POLAR_OK;
+}
+
+polar_status polar_p2p_probe(polar_comm_t comm, void* const* bufs, size_t bytes, int iters, polar_p2p_result* out) {
+    if (!comm || !bufs || !out || bytes < 16 || bytes % 16 || iters < 1) return POLAR_EINVAL;
+    polar_status st = check_latched(comm);
+    if (st != POLAR_OK) return st;
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
+    dev::Params P;
+    fill_params(comm, P);
+    int nch = POLAR_MAXCH;
+    if (comm->is_virtual) nch = std::max(1, std::min(nch, comm->max_coop_blocks / comm->nranks));
+    P.nch = nch;
+    P.count = bytes;
+    P.vec = 1;
+    if (comm->is_virtual) {
+        for (int p = 0; p < comm->nranks; ++p) {
+            if (!bufs[p] || reinterpret_cast<uintptr_t>(bufs[p]) % 16) return POLAR_EINVAL;
+            P.bufs[p] = static_cast<char*>(bufs[p]);
+        }
+    } else {
+        const Registration* reg = find_reg(comm, static_cast<const char*>(bufs[0]), bytes);
+        if (!reg || reinterpret_cast<uintptr_t>(bufs[0]) % 16) return POLAR_EINVAL;
+        const size_t off = (size_t)(static_cast<const char*>(bufs[0]) - reg->base);
+        for (int p = 0; p < comm->nranks; ++p) P.bufs[p] = reg->peer[p] + off;
+    }
+    const int grid = comm->nlocal * nch;
+    unsigned long long *times = nullptr, *sums = nullptr;
+    if (cudaMalloc(&times, sizeof(unsigned long long) * 2 * grid) != cudaSuccess) return POLAR_ENOMEM;
+    if (cudaMalloc(&sums, sizeof(unsigned long long) * grid) != cudaSuccess) { cudaFree(times); return POLAR_ENOMEM; }
+    std::vector<unsigned long long> ht(2 * grid);
+    for (int l = 0; l < comm->nlocal; ++l) out[l] = polar_p2p_result{};
+    for (int mode = dev::PROBE_LOAD; mode <= dev::PROBE_PINGPONG && st == POLAR_OK; ++mode) {
+        unsigned long long epoch = ++comm->probe_epoch;
+        void* args[] = {&P, &mode, &iters, &epoch, &times, &sums};
+        cudaError_t e = comm->is_virtual
+                            ? cudaLaunchCooperativeKernel((const void*)dev::p2p_probe_kernel, dim3(grid), dim3(dev::kBlock), args, 0, 0)
+                            : cudaLaunchKernel((const void*)dev::p2p_probe_kernel, dim3(grid), dim3(dev::kBlock), args, 0, 0);
+        if (e != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) { st = POLAR_ECUDA; break; }
+        comm->launches++;
+        st = check_latched(comm);
+        if (st != POLAR_OK) break;
+        if (cudaMemcpy(ht.data(), times, sizeof(unsigned long long) * 2 * grid, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            st = POLAR_ECUDA;
+            break;
+        }
+        for (int l = 0; l < comm->nlocal; ++l) {
+            unsigned long long t0 = ~0ull, t1 = 0;
+            for (int ch = 0; ch < nch; ++ch) {
+                t0 = std::min(t0, ht[2 * (l * nch + ch)]);
+                t1 = std::max(t1, ht[2 * (l * nch + ch) + 1]);
+            }
+            const double ns = (double)(t1 - t0);
+            if (mode == dev::PROBE_LOAD) out[l].load_gbs = ns > 0 ? (double)bytes * iters / ns : 0.0;
+            if (mode == dev::PROBE_STORE) out[l].store_gbs = ns > 0 ? (double)bytes * iters / ns : 0.0;
+            if (mode == dev::PROBE_PINGPONG) {
+                const int r = comm->rank0 + l;
+                const double pp = (double)(ht[2 * (l * nch) + 1] - ht[2 * (l * nch)]);
+                out[l].pingpong_us = (r ^ 1) < comm->nranks ? pp / iters / 1e3 : 0.0;
+            }
+        }
+        if (mode == dev::PROBE_LOAD) {
+            std::vector<unsigned long long> hs(grid);
+            cudaMemcpy(hs.data(), sums, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+            for (int l = 0; l < comm->nlocal; ++l) {
+                unsigned long long x = 0;
+                for (int ch = 0; ch < nch; ++ch) x ^= hs[l * nch + ch];
+                out[l].load_xor = x;
+            }
+        }
+    }
+    cudaFree(times);
+    cudaFree(sums);
+    return st;
 }
 
 const char* polar_version(void) { return "polar 0.1 sm_100a"; }

@@ -30,7 +30,10 @@ enum FlagKind : int {
     F_TREE_DTAIL = 7,  // tree down: parent -> child, slot 0
     F_TREE_DHEAD = 8,  // tree down: child k -> parent, slot k
     F_INIT = 9,        // init barrier
-    F_NKINDS = 10
+    F_PROBE_ENTRY = 10,  // p2p probe: entry barrier (slot = source rank)
+    F_PROBE_EXIT = 11,   // p2p probe: exit barrier
+    F_PROBE_PP = 12,     // p2p probe: ping-pong flag (channel 0, slot 0)
+    F_NKINDS = 13
 };
 constexpr size_t kFlagRow = 128;  // bytes per (kind, channel) row
 constexpr size_t kFlagBytes = (size_t)F_NKINDS * kMaxCh * kFlagRow;

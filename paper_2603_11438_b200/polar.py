@@ -127,6 +127,7 @@ _sigs = {
     "polar_comm_launch_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "polar_comm_check": (C.c_int, [_P]),
     "polar_comm_set_trace": (C.c_int, [_P, _P, C.c_size_t]),
+    "polar_p2p_probe": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, _P]),
     "polar_bench_enqueue": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P, C.c_uint64,
                                       C.POINTER(C.c_double)]),
     "polar_adaptive_config": (C.c_int, [_P, C.POINTER(AdaptiveParams)]),
@@ -279,6 +280,11 @@ def bootstrap_check(nranks: int, rank: int, allgather) -> int:
     return lib.polar_bootstrap_check(nranks, rank, cb, None)
 
 
+class _P2PResult(C.Structure):
+    _fields_ = [("load_gbs", C.c_double), ("store_gbs", C.c_double), ("pingpong_us", C.c_double),
+                ("load_xor", C.c_ulonglong)]
+
+
 class Comm:
     """A communicator: ``Comm.virtual(n)`` (n ranks on one GPU) or
     ``Comm.init(n, rank, device, allgather)`` (one rank per process)."""
@@ -389,6 +395,18 @@ class Comm:
         darr, _, _ = self._bufs(dev_tensors)
         _check(lib.polar_allreduce_host(self.h, harr, darr, n, dt, OP_CODES[op], _stream_ptr(stream)),
                "polar_allreduce_host")
+
+    def p2p_probe(self, tensors, iters=5):
+        """Collective peer-path probe (polar.h polar_p2p_probe): per local rank a dict
+        {load_gbs, store_gbs, pingpong_us, load_xor}; tensors are the symmetric
+        buffers (whole tensors, 16-B multiple)."""
+        arr, _, _ = self._bufs(tensors)
+        nbytes = tensors[0].numel() * tensors[0].element_size() if isinstance(tensors, (list, tuple)) else \
+            tensors.numel() * tensors.element_size()
+        res = (_P2PResult * self.nlocal)()
+        _check(lib.polar_p2p_probe(self.h, arr, nbytes, int(iters), C.cast(res, C.c_void_p)), "polar_p2p_probe")
+        return [{"load_gbs": r.load_gbs, "store_gbs": r.store_gbs, "pingpong_us": r.pingpong_us,
+                 "load_xor": r.load_xor} for r in res]
 
     def bench_enqueue(self, tensors, ncalls=2000, op="sum", stream=None) -> float:
         """Host ns per polar_allreduce_v call (decide + dispatch + launch), native loop."""

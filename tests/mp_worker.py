@@ -118,6 +118,23 @@ def main():
     st = L.lib.polar_broadcast(comm.h, L.C.c_void_p(plain.data_ptr()), rc, L.FLOAT32, 0,
                                L.C.c_void_p(torch.cuda.current_stream().cuda_stream))
     results.append({"tag": "bc/unregistered-einval", "rank": rank, "ok": st == L.EINVAL, "identical": True})
+    # p2p probe over the IPC peer mapping: loads of peer (r+1)%n checked by XOR,
+    # stores checked in my own buffer (written by rank (r-1)%n)
+    (pb,) = comm.mem_alloc_tensors((256 << 10) // 4, torch.int32)
+    pb.copy_(torch.from_numpy(synth.gen("i32", (256 << 10) // 4, rank, cfg=35, dist="full")))
+    torch.cuda.synchronize()
+    peer_before = synth.gen("i32", (256 << 10) // 4, (rank + 1) % ws, cfg=35, dist="full").view(np.uint32)
+    w = peer_before.reshape(-1, 4).astype(np.uint64)
+    exp_xor = int(np.bitwise_xor.reduce(((w[:, 0] ^ w[:, 2]) << np.uint64(32)) | (w[:, 1] ^ w[:, 3])))
+    (pr,) = comm.p2p_probe(pb, iters=3)
+    mine = pb.cpu().numpy().view(np.uint32).reshape(-1, 4)
+    writer = (rank - 1) % ws
+    i = np.arange(mine.shape[0], dtype=np.uint64)
+    pat_ok = (np.array_equal(mine[:, 0], (i & np.uint64(0xFFFFFFFF)).astype(np.uint32)) and
+              bool((mine[:, 2] == writer).all()) and np.array_equal(mine[:, 3], ~mine[:, 0]))
+    results.append({"tag": "p2p_probe", "rank": rank, "identical": True,
+                    "ok": bool(pr["load_xor"] == exp_xor and pat_ok and pr["load_gbs"] > 0 and pr["store_gbs"] > 0
+                               and (pr["pingpong_us"] > 0) == ((rank ^ 1) < ws))})
     # collective free of a symmetric buffer, then a fresh allocation still works
     sym_ptr = sym.data_ptr()
     del sym, sym_i, bc

@@ -120,3 +120,37 @@ def test_unsupported_decision_and_bad_root():
         assert e.value.name == "eunsupported"
     finally:
         L.set_policy([])
+
+
+def _fold_xor(arr_u32):
+    w = arr_u32.reshape(-1, 4).astype(np.uint64)
+    return int(np.bitwise_xor.reduce(((w[:, 0] ^ w[:, 2]) << np.uint64(32)) | (w[:, 1] ^ w[:, 3])))
+
+
+def _pattern(npacks, writer):
+    i = np.arange(npacks, dtype=np.uint64)
+    p = np.empty((npacks, 4), dtype=np.uint32)
+    p[:, 0] = (i & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    p[:, 1] = ((i >> np.uint64(32)).astype(np.uint32)) ^ np.uint32(0x9E3779B9)
+    p[:, 2] = writer
+    p[:, 3] = ~p[:, 0]
+    return p.reshape(-1)
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_p2p_probe_virtual(n):
+    """polar_p2p_probe: every rank reads peer (r+1)%n (checked by the
+    XOR of the packs it loaded), writes the pattern into it (checked in the peer
+    buffer afterwards) and bounces a flag with r^1; rates and latencies are > 0."""
+    nbytes = (1 << 20) + 4096
+    c = comm(n)
+    bufs = [torch.randint(-2**31, 2**31 - 1, (nbytes // 4,), dtype=torch.int32, device="cuda") for _ in range(n)]
+    before = [b.cpu().numpy().view(np.uint32).copy() for b in bufs]
+    res = c.p2p_probe(bufs, iters=3)
+    for r in range(n):
+        peer = (r + 1) % n
+        assert res[r]["load_xor"] == _fold_xor(before[peer]), r
+        assert res[r]["load_gbs"] > 0 and res[r]["store_gbs"] > 0
+        assert (res[r]["pingpong_us"] > 0) == ((r ^ 1) < n)
+        got = bufs[peer].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, _pattern(nbytes // 16, r)), r
