@@ -277,3 +277,40 @@ def test_allreduce_host_chunk_pipeline(chunk, monkeypatch):
             for h in host:
                 got = h.view(torch.int16).numpy() if dtype == "bf16" else h.numpy()
                 assert np.array_equal(got.view(np.uint8), exp.view(np.uint8))
+
+
+@pytest.mark.parametrize("algo,proto", [("twoshot", "simple"), ("ring", "simple"), ("twoshot", "ll128")])
+def test_beyond_2pow31_elements(algo, proto):
+    """Maximum sizes: 2^31 + 1003 f32 elements per rank (8 GiB, the paper's largest
+    Table-2 size) — every index past 2^31 must be 64-bit.  Inputs are a
+    formula evaluated on the device; sampled windows (including the ragged end)
+    are checked against the oracle on the same formula evaluated on the host."""
+    from oracle import allreduce as orc
+    n, count = 2, (1 << 31) + 1003
+
+    def host(r, lo, hi):
+        i = np.arange(lo, hi, dtype=np.int64)
+        return (((i * 2654435761 + 977 * r) % 1021) - 510).astype(np.float32)
+
+    ts = []
+    for r in range(n):
+        t = torch.empty(count, dtype=torch.float32, device="cuda")
+        step = 1 << 28
+        for lo in range(0, count, step):
+            hi = min(count, lo + step)
+            i = torch.arange(lo, hi, dtype=torch.int64, device="cuda")
+            t[lo:hi] = (((i * 2654435761 + 977 * r) % 1021) - 510).to(torch.float32)
+            del i
+        ts.append(t)
+    c = comm(n)
+    try:
+        c.allreduce_forced(ts, algo, proto, 32)
+        torch.cuda.synchronize()
+        c.check()
+        for lo, hi in ((0, 4096), ((1 << 31) - 2048, (1 << 31) + 1000), (count - 5000, count), (1 << 30, (1 << 30) + 999)):
+            exp = orc.allreduce([host(r, lo, hi) for r in range(n)], "f32", "sum")
+            for t in ts:
+                assert np.array_equal(t[lo:hi].cpu().numpy(), exp), (lo, hi)
+    finally:
+        del ts
+        torch.cuda.empty_cache()
