@@ -20,9 +20,6 @@ namespace dev {
 #ifndef POLAR_LB_MIN
 #define POLAR_LB_MIN 1      // min resident CTAs per SM requested from ptxas (register cap; 2 spills)
 #endif
-#ifndef POLAR_TS_UNROLL
-#define POLAR_TS_UNROLL 1   // packs per thread per two-shot iteration
-#endif
 constexpr int kBlock = POLAR_BLOCK;   // threads per CTA (one CTA per rank-channel)
 
 struct Params {

@@ -295,6 +295,23 @@ __device__ void twoshot_tma(const Params& P, const Who& w, const TwoShotGeo& g) 
     }
 }
 
+// owner j's shard of the zero-copy two-shot as a chunk queue: big chunks first,
+// then small ones for the last nch * kTsBig packs (balanced tail)
+template <int ES>
+__device__ __forceinline__ TwoShotGeo twoshot_geo(const Params& P, int j, uint64_t e) {
+    TwoShotGeo g;
+    split_range(0, npacks<ES>(P), P.nranks, j, g.s0, g.s1);
+    const unsigned long long L = g.s1 - g.s0;
+    const unsigned long long tail = L < (unsigned long long)P.nch * kTsBig ? L : (unsigned long long)P.nch * kTsBig;
+    g.nbig = (L - tail) / kTsBig;
+    g.bigend = g.nbig * kTsBig;
+    g.nchunks = g.nbig + (L - g.bigend + kTsSmall - 1) / kTsSmall;
+    g.nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
+    g.work = reinterpret_cast<unsigned long long*>(&chan_state(P, j, 0)->work);
+    g.wbase = (unsigned long long)e << 32;
+    return g;
+}
+
 template <int DT, int OP>
 __device__ void twoshot_simple(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
@@ -314,17 +331,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     // SM takes fewer chunks (static slices left a ~15 % loop-time spread,
     // measured with polar_comm_set_trace).  Big chunks first, then small ones
     // for the last nch*kTsBig packs so the tail is balanced too.
-    TwoShotGeo g;
-    const unsigned long long NP = npacks<ES>(P);
-    split_range(0, NP, n, w.r, g.s0, g.s1);
-    const unsigned long long L = g.s1 - g.s0;
-    const unsigned long long tail = L < (unsigned long long)P.nch * kTsBig ? L : (unsigned long long)P.nch * kTsBig;
-    g.nbig = (L - tail) / kTsBig;
-    g.bigend = g.nbig * kTsBig;
-    g.nchunks = g.nbig + (L - g.bigend + kTsSmall - 1) / kTsSmall;
-    g.nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
-    g.work = reinterpret_cast<unsigned long long*>(&chan_state(P, w.r, 0)->work);
-    g.wbase = (unsigned long long)e << 32;
+    const TwoShotGeo g = twoshot_geo<ES>(P, w.r, e);
     if (P.tma && P.vec) {
         twoshot_tma<DT, OP>(P, w, g);
     } else switch (n) {
