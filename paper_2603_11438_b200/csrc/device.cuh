@@ -264,22 +264,37 @@ __device__ __forceinline__ bool wait_geq(const Params& P, const uint64_t* p, uin
     return wait_geq_slow(p, v, P.sys, P.timeout_ns, P.err);
 }
 
-// Poll one LL line until both flags equal `flag`; false on timeout.
+// Poll one LL line until both flags equal `flag`; false on timeout.  The spin is
+// out of line with by-value arguments (code size where many polls are inlined,
+// and no address of the kernel's Params is taken).
+struct PollRes {
+    uint4 v;
+    int ok;
+};
+static __device__ __noinline__ PollRes poll_ll_slow(const uint4* p, uint32_t flag, unsigned long long timeout_ns,
+                                                   int* err) {
+    PollRes r;
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1;; ++it) {
+        r.v = ld_ll(p);
+        if (r.v.y == flag && r.v.w == flag) { r.ok = 1; return r; }
+        if ((it & 1023) == 0) {
+            if (globaltimer() - t0 > timeout_ns) {
+                *(volatile int*)err = POLAR_ETIMEOUT;
+                __threadfence_system();
+                r.ok = 0;
+                return r;
+            }
+            if (*(volatile int*)err) { r.ok = 0; return r; }
+        }
+    }
+}
 __device__ __forceinline__ bool poll_ll(const Params& P, const uint4* p, uint32_t flag, uint4& out) {
     uint4 v = ld_ll(p);
     if (v.y == flag && v.w == flag) { out = v; return true; }
-    const uint64_t t0 = globaltimer();
-    for (uint32_t it = 1;; ++it) {
-        v = ld_ll(p);
-        if (v.y == flag && v.w == flag) { out = v; return true; }
-        if ((it & 1023) == 0) {
-            if (globaltimer() - t0 > P.timeout_ns) {
-                raise_error(P, POLAR_ETIMEOUT);
-                return false;
-            }
-            if (*(volatile int*)P.err) return false;
-        }
-    }
+    const PollRes r = poll_ll_slow(p, flag, P.timeout_ns, P.err);
+    out = r.v;
+    return r.ok != 0;
 }
 
 // LL128 reader helpers: does this lane's 16 B of a line group carry `flag`
@@ -303,9 +318,12 @@ __device__ __forceinline__ uint4 ll128_unpack(const uint4& w) {
 }
 
 // Poll one LL128 line group until all four flags equal `flag`, then unpack.
-// Warp-uniform result; false on timeout (error latched).
-__device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, uint64_t flag, uint4& out) {
+// Warp-uniform result; false on timeout (error latched).  Out of line with
+// by-value arguments like poll_ll_slow; warp-collective.
+static __device__ __noinline__ PollRes ld_ll128_slow(const uint4* group, uint64_t flag, unsigned long long timeout_ns,
+                                                    int* err) {
     const int lane = (int)(threadIdx.x & 31);
+    PollRes r;
     uint4 w;
     uint64_t t0 = 0;
     for (uint32_t it = 0;; ++it) {
@@ -316,14 +334,25 @@ __device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, ui
             if (lane == 0) {
                 const uint64_t now = globaltimer();
                 if (t0 == 0) t0 = now;
-                if (now - t0 > P.timeout_ns) { raise_error(P, POLAR_ETIMEOUT); bad = 1; }
-                else if (*(volatile int*)P.err) bad = 1;
+                if (now - t0 > timeout_ns) {
+                    *(volatile int*)err = POLAR_ETIMEOUT;
+                    __threadfence_system();
+                    bad = 1;
+                } else if (*(volatile int*)err) {
+                    bad = 1;
+                }
             }
-            if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+            if (__shfl_sync(0xffffffffu, bad, 0)) { r.ok = 0; r.v = w; return r; }
         }
     }
-    out = ll128_unpack(w);
-    return true;
+    r.v = ll128_unpack(w);
+    r.ok = 1;
+    return r;
+}
+__device__ __forceinline__ bool ld_ll128(const Params& P, const uint4* group, uint64_t flag, uint4& out) {
+    const PollRes r = ld_ll128_slow(group, flag, P.timeout_ns, P.err);
+    out = r.v;
+    return r.ok != 0;
 }
 
 // ------------------------------------------------------------ scratch access

@@ -376,6 +376,9 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
 #ifndef POLAR_BATCH_LL
 #define POLAR_BATCH_LL 2
 #endif
+#ifndef POLAR_UR_LL128
+#define POLAR_UR_LL128 1    // LL128 units per warp in the one-/two-shot reduce (fold_peers)
+#endif
 template <int PROTO> __host__ __device__ constexpr int batch_for() {
     return PROTO == POLAR_PROTO_SIMPLE ? POLAR_BATCH_SIMPLE : POLAR_BATCH_LL;
 }
@@ -391,60 +394,55 @@ template <int U> struct Batch {
 
 template <int PROTO> struct Wire;
 
+// Each wire splits a get into issue() (the loads, no waiting), ready() (did this
+// thread's copy arrive), decode() and poll() (wait and load again).  Callers issue
+// a whole batch — or the same pack from every peer — check readiness once, and
+// only if something had not arrived yet fall back to polling each wire index from
+// scratch (so no raw value stays live across the out-of-line spin loops).
+
 template <> struct Wire<POLAR_PROTO_SIMPLE> {
     static constexpr unsigned long long kPacks = 1;   // packs per wire index (per thread)
+    struct Raw { uint4 a; };
     static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) { return slot_bytes / 16; }
     static __device__ __forceinline__ void put(const Params&, uint4* slot, unsigned long long k, uint4 v, uint64_t) {
         st_plain(slot + k, v);
     }
-    template <int U, int NW>
-    static __device__ __forceinline__ bool get_batch(const Params&, const uint4* slot, const Batch<U>& b, uint64_t,
-                                                     uint4 (&v)[U][NW]) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < NW; ++q)
-                if (b.in[u]) v[u][q] = ld_cg(slot + b.j[u] * NW + q);
+    static __device__ __forceinline__ void issue(const uint4* slot, unsigned long long k, Raw& r) { r.a = ld_cg(slot + k); }
+    static __device__ __forceinline__ bool ready(const Raw&, uint64_t) { return true; }
+    static __device__ __forceinline__ uint4 decode(const Raw& r) { return r.a; }
+    static __device__ __forceinline__ bool poll(const Params&, const uint4* slot, unsigned long long k, uint64_t, uint4& v) {
+        v = ld_cg(slot + k);
         return true;
     }
 };
 template <> struct Wire<POLAR_PROTO_LL> {
     static constexpr unsigned long long kPacks = 1;
+    struct Raw { uint4 a, b; };
     static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) { return slot_bytes / 32; }
     static __device__ __forceinline__ void put(const Params& P, uint4* slot, unsigned long long k, uint4 v, uint64_t f) {
         jitter(P), st_ll(slot + 2 * k, v.x, v.y, (uint32_t)f);
         jitter(P), st_ll(slot + 2 * k + 1, v.z, v.w, (uint32_t)f);
     }
-    template <int U, int NW>
-    static __device__ __forceinline__ bool get_batch(const Params& P, const uint4* slot, const Batch<U>& b, uint64_t f,
-                                                     uint4 (&v)[U][NW]) {
+    static __device__ __forceinline__ void issue(const uint4* slot, unsigned long long k, Raw& r) {
+        r.a = ld_ll(slot + 2 * k);
+        r.b = ld_ll(slot + 2 * k + 1);
+    }
+    static __device__ __forceinline__ bool ready(const Raw& r, uint64_t f) {
         const uint32_t fl = (uint32_t)f;
-        uint4 l[U][NW][2];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < NW; ++q)
-                if (b.in[u]) {
-                    l[u][q][0] = ld_ll(slot + 2 * (b.j[u] * NW + q));
-                    l[u][q][1] = ld_ll(slot + 2 * (b.j[u] * NW + q) + 1);
-                }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < NW; ++q)
-                if (b.in[u]) {
-                    const uint4* p = slot + 2 * (b.j[u] * NW + q);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        if (l[u][q][h].y != fl || l[u][q][h].w != fl)
-                            if (!poll_ll(P, p + h, fl, l[u][q][h])) return false;
-                    v[u][q] = make_uint4(l[u][q][0].x, l[u][q][0].z, l[u][q][1].x, l[u][q][1].z);
-                }
+        return r.a.y == fl && r.a.w == fl && r.b.y == fl && r.b.w == fl;
+    }
+    static __device__ __forceinline__ uint4 decode(const Raw& r) { return make_uint4(r.a.x, r.a.z, r.b.x, r.b.z); }
+    static __device__ __forceinline__ bool poll(const Params& P, const uint4* slot, unsigned long long k, uint64_t f,
+                                                uint4& v) {
+        uint4 l0, l1;
+        if (!poll_ll(P, slot + 2 * k, (uint32_t)f, l0) || !poll_ll(P, slot + 2 * k + 1, (uint32_t)f, l1)) return false;
+        v = make_uint4(l0.x, l0.z, l1.x, l1.z);
         return true;
     }
 };
 template <> struct Wire<POLAR_PROTO_LL128> {
     static constexpr unsigned long long kPacks = kLL128Packs;
+    struct Raw { uint4 a; };
     static __device__ __forceinline__ unsigned long long units(unsigned long long slot_bytes) {
         return slot_bytes / kLL128UnitBytes;
     }
@@ -453,31 +451,106 @@ template <> struct Wire<POLAR_PROTO_LL128> {
         __syncwarp();
         st_ll128(slot + (kLL128UnitBytes / 16) * k, v, f);
     }
-    template <int U, int NW>
-    static __device__ __forceinline__ bool get_batch(const Params& P, const uint4* slot, const Batch<U>& b, uint64_t f,
-                                                     uint4 (&v)[U][NW]) {
-        const unsigned lane = threadIdx.x & 31;
-        uint4 w[U][NW];
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < NW; ++q)
-                if (b.in[u]) w[u][q] = ld_ll(slot + (kLL128UnitBytes / 16) * (b.j[u] * NW + q) + lane);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < NW; ++q)
-                if (b.in[u]) {
-                    if (__all_sync(0xffffffffu, ll128_lane_ready(w[u][q], f))) {
-                        v[u][q] = ll128_unpack(w[u][q]);
-                    } else if (!ld_ll128(P, slot + (kLL128UnitBytes / 16) * (b.j[u] * NW + q), f, v[u][q])) {
-                        return false;
-                    }
-                }
-        return true;
+    // warp-collective: every lane issues its 16 B of the line group; ready() is
+    // per lane (the caller votes), decode() shuffles
+    static __device__ __forceinline__ void issue(const uint4* slot, unsigned long long k, Raw& r) {
+        r.a = ld_ll(slot + (kLL128UnitBytes / 16) * k + (threadIdx.x & 31));
+    }
+    static __device__ __forceinline__ bool ready(const Raw& r, uint64_t f) { return ll128_lane_ready(r.a, f); }
+    static __device__ __forceinline__ uint4 decode(const Raw& r) { return ll128_unpack(r.a); }
+    static __device__ __forceinline__ bool poll(const Params& P, const uint4* slot, unsigned long long k, uint64_t f,
+                                                uint4& v) {
+        return ld_ll128(P, slot + (kLL128UnitBytes / 16) * k, f, v);
     }
 };
+
+// all-arrived vote: per thread, or per warp for LL128 (whose get is warp-collective)
+template <int PROTO> __device__ __forceinline__ bool all_ready(bool mine) {
+    if constexpr (PROTO == POLAR_PROTO_LL128) return __all_sync(0xffffffffu, mine);
+    return mine;
+}
+
+// a batch's NW wire words per pack from one slot
+template <int PROTO, int U, int NW>
+__device__ __forceinline__ bool get_batch(const Params& P, const uint4* slot, const Batch<U>& b, uint64_t f,
+                                          uint4 (&v)[U][NW]) {
+    using W = Wire<PROTO>;
+    if (PROTO == POLAR_PROTO_LL128) __syncwarp();
+    {
+        typename W::Raw raw[U][NW];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) W::issue(slot, b.j[u] * NW + q, raw[u][q]);
+        bool rd = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (b.in[u]) rd = rd && W::ready(raw[u][q], f);
+        if (all_ready<PROTO>(rd)) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < NW; ++q)
+                    if (b.in[u]) v[u][q] = W::decode(raw[u][q]);
+            return true;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < NW; ++q)
+            if (b.in[u] && !W::poll(P, slot, b.j[u] * NW + q, f, v[u][q])) return false;
+    return true;
+}
+
+// Fold the same batch from every rank in rank order: fold(p, u, x) is called for
+// p = 0..n-1 (x = own[u] for p == self, else rank p's copy from slot(p)).  All
+// loads of all peers are issued first and checked with one vote — one wait for
+// n-1 senders instead of n-1 waits; if something has not arrived yet, peers are
+// polled one by one in rank order and folded as they arrive (so only the
+// accumulators stay live across the out-of-line spin loops).
+template <int PROTO, int U, class SlotFn, class Fold>
+__device__ __forceinline__ bool fold_peers(const Params& P, SlotFn&& slot, int self, int n, const Batch<U>& b,
+                                           uint64_t f, const uint4 (&own)[U], Fold&& fold) {
+    using W = Wire<PROTO>;
+    if (PROTO == POLAR_PROTO_LL128) __syncwarp();
+    {
+        typename W::Raw raw[kMaxRanks][U];
+#pragma unroll
+        for (int p = 0; p < kMaxRanks; ++p)
+            if (p < n && p != self)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b.in[u]) W::issue(slot(p), b.j[u], raw[p][u]);
+        bool rd = true;
+#pragma unroll
+        for (int p = 0; p < kMaxRanks; ++p)
+            if (p < n && p != self)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b.in[u]) rd = rd && W::ready(raw[p][u], f);
+        if (all_ready<PROTO>(rd)) {
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < n)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) fold(p, u, p == self ? own[u] : W::decode(raw[p][u]));
+            return true;
+        }
+    }
+#pragma unroll 1
+    for (int p = 0; p < n; ++p)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint4 x = own[u];
+            if (p != self && b.in[u] && !W::poll(P, slot(p), b.j[u], f, x)) return false;
+            fold(p, u, x);
+        }
+    return true;
+}
 
 // Run body(batch) over packs [lo, hi) in batches of U (see Batch).  The body
 // returns false to stop (timeout); so does for_batch.  For LL128 the whole warp
@@ -554,6 +627,7 @@ template <int DT, int OP, int PROTO>
 __device__ void twoshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int U = batch_for<PROTO>();
+    constexpr int UR = PROTO == POLAR_PROTO_LL ? 1 : POLAR_UR_LL128;   // fold_peers holds n-1 raw copies per pack
     using W = Wire<PROTO>;
     const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
@@ -581,30 +655,25 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
                 return true;
             });
         }
-        // reduce my part in rank order, keep it and push it to every rank
+        // reduce my part in rank order, keep it and push it to every rank; every
+        // sender's staging is polled at once (fold_peers); own part only, so this
+        // loop may use its own batch (UR) without a barrier
         geo_slice(g, NP, k, w.r, w.c, lo, hi, off);
         const unsigned long long ob = off / W::kPacks;
-        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
-            const Batch<U> sb = shifted(b, ob);
-            uint4 own[U];
+        ok = for_batch<PROTO, UR>(lo, hi, [&](const Batch<UR>& b) {
+            const Batch<UR> sb = shifted(b, ob);
+            uint4 own[UR];
             load_batch<ES>(P, mine, b, own);
-            Acc<DT> acc[U];
-            for (int p = 0; p < n; ++p) {
-                uint4 v[U][1];
-                if (p == w.r) {
+            Acc<DT> acc[UR];
+            if (!fold_peers<PROTO, UR>(
+                    P, [&](int p) -> const uint4* { return ts_stage<PROTO>(P, w.r, 0, par, p); }, w.r, n, sb, e, own,
+                    [&](int p, int u, const uint4& x) {
+                        if (p == 0) acc_init<DT>(acc[u], x);
+                        else acc_add<DT, OP>(acc[u], x);
+                    }))
+                return false;
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u][0] = own[u];
-                } else if (!W::template get_batch<U, 1>(P, ts_stage<PROTO>(P, w.r, 0, par, p), sb, e, v)) {
-                    return false;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (p == 0) acc_init<DT>(acc[u], v[u][0]);
-                    else acc_add<DT, OP>(acc[u], v[u][0]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
+            for (int u = 0; u < UR; ++u) {
                 if (!b.in[u]) continue;
                 const uint4 out = acc_fin<DT>(acc[u]);
                 if (b.act[u]) store_pack<ES>(P, mine, b.i[u], out);
@@ -621,7 +690,7 @@ __device__ void twoshot_ll(const Params& P, const Who& w) {
             const unsigned long long obj = off / W::kPacks;
             ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
                 uint4 v[U][1];
-                if (!W::template get_batch<U, 1>(P, src, shifted(b, obj), e, v)) return false;
+                if (!get_batch<PROTO, U, 1>(P, src, shifted(b, obj), e, v)) return false;
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (b.act[u]) store_pack<ES>(P, mine, b.i[u], v[u][0]);
@@ -702,6 +771,7 @@ template <int DT, int OP, int PROTO>
 __device__ void oneshot_ll(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int U = batch_for<PROTO>();
+    constexpr int UR = PROTO == POLAR_PROTO_LL ? 1 : POLAR_UR_LL128;   // fold_peers holds n-1 raw copies per pack
     using W = Wire<PROTO>;
     const int n = w.n;
     ChanState* st = chan_state(P, w.r, w.c);
@@ -726,27 +796,21 @@ __device__ void oneshot_ll(const Params& P, const Who& w) {
                         if (p != w.r) W::put(P, osll_slot<PROTO>(P, p, par, w.r), ob + b.j[u], v[u], e);
             return true;
         });
-        ok = for_batch<PROTO, U>(lo, hi, [&](const Batch<U>& b) {
-            const Batch<U> sb = shifted(b, ob);
-            uint4 own[U];
+        __syncthreads();   // every push has read `mine` before the reduce below (another batch) writes it
+        ok = for_batch<PROTO, UR>(lo, hi, [&](const Batch<UR>& b) {
+            const Batch<UR> sb = shifted(b, ob);
+            uint4 own[UR];
             load_batch<ES>(P, mine, b, own);
-            Acc<DT> acc[U];
-            for (int p = 0; p < n; ++p) {
-                uint4 v[U][1];
-                if (p == w.r) {
+            Acc<DT> acc[UR];
+            if (!fold_peers<PROTO, UR>(
+                    P, [&](int p) -> const uint4* { return osll_slot<PROTO>(P, w.r, par, p); }, w.r, n, sb, e, own,
+                    [&](int p, int u, const uint4& x) {
+                        if (p == 0) acc_init<DT>(acc[u], x);
+                        else acc_add<DT, OP>(acc[u], x);
+                    }))
+                return false;
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u][0] = own[u];
-                } else if (!W::template get_batch<U, 1>(P, osll_slot<PROTO>(P, w.r, par, p), sb, e, v)) {
-                    return false;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (p == 0) acc_init<DT>(acc[u], v[u][0]);
-                    else acc_add<DT, OP>(acc[u], v[u][0]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int u = 0; u < UR; ++u)
                 if (b.act[u]) store_pack<ES>(P, mine, b.i[u], acc_fin<DT>(acc[u]));
             return true;
         });
@@ -841,7 +905,7 @@ __device__ void ring(const Params& P, const Who& w) {
                     }
                 } else if (s < n) {
                     uint4 in[U][AW];
-                    if (!W::template get_batch<U, AW>(P, src, b, fin, in)) return false;
+                    if (!get_batch<PROTO, U, AW>(P, src, b, fin, in)) return false;
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (!b.in[u]) continue;
@@ -860,7 +924,7 @@ __device__ void ring(const Params& P, const Who& w) {
                     }
                 } else {
                     uint4 v[U][1];
-                    if (!W::template get_batch<U, 1>(P, src, b, fin, v)) return false;
+                    if (!get_batch<PROTO, U, 1>(P, src, b, fin, v)) return false;
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (!b.in[u]) continue;
@@ -961,7 +1025,7 @@ __device__ void tree(const Params& P, const Who& w) {
             for (int u = 0; u < U; ++u) acc_init<DT>(acc[u], own[u]);
             for (int k = 0; k < nchild; ++k) {
                 uint4 in[U][AW];
-                if (!W::template get_batch<U, AW>(P, tree_up_slot<PROTO>(P, r, c, k, urecv[k]), b, urecv[k] + 1, in))
+                if (!get_batch<PROTO, U, AW>(P, tree_up_slot<PROTO>(P, r, c, k, urecv[k]), b, urecv[k] + 1, in))
                     return false;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -1015,7 +1079,7 @@ __device__ void tree(const Params& P, const Who& w) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) v[u][0] = own[u];
             } else {
-                if (!W::template get_batch<U, 1>(P, src, b, fin, v)) return false;
+                if (!get_batch<PROTO, U, 1>(P, src, b, fin, v)) return false;
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (b.act[u]) store_pack<ES>(P, mine, b.i[u], v[u][0]);

@@ -1,0 +1,12 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+export POLAR_TIMEOUT_MS=5000
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_faults.py -q -x -k "ll or edges or multi_chunk or back_to_back or jitter" --timeout=600 2>&1 | tail -2
+for L in cur old ur2; do
+  if [ $L = cur ]; then unset POLAR_LIB; else export POLAR_LIB=build/variants/libpolar_$L.so; fi
+  timeout 600 python scripts/sweep.py --n 8 --dtype f32 --sizes 1K,16K,256K,1M,16M --algos oneshot:ll128,twoshot:ll128 --nch 4,16 --graph --iters 20 > gpurun_out/llp_$L.jsonl 2>&1
+  python -c "
+import json
+r=[json.loads(l) for l in open('gpurun_out/llp_$L.jsonl') if l.startswith('{')]
+print('$L', [(x['algo']+':'+x['proto'], x['bytes'], x['nch'], x.get('us')) for x in r])"
+done
