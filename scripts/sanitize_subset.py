@@ -1,0 +1,52 @@
+"""Small parity subset for compute-sanitizer (memcheck / racecheck / synccheck):
+every algorithm x protocol, f32 + bf16, ragged counts, 3 virtual ranks, the TMA
+two-shot, the direct collectives and the p2p probe; exits non-zero on a mismatch."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from oracle import allreduce as orc  # noqa: E402
+from paper_2603_11438_b200 import polar as L  # noqa: E402
+from tests.gpu_common import to_device, to_host  # noqa: E402
+
+n = 3
+c = L.Comm.virtual(n, 0)
+bad = 0
+for dtype in ("f32", "bf16"):
+    for algo in ("oneshot", "twoshot", "ring", "tree"):
+        for proto in ("ll", "ll128", "simple"):
+            for count in (7, 5003):
+                xs = synth.gen_ranks(dtype, count, n, cfg=5, dist="ints")
+                ts = [to_device(x, dtype) for x in xs]
+                c.allreduce_forced(ts, algo, proto, 2)
+                torch.cuda.synchronize()
+                c.check()
+                exp = orc.allreduce(xs, dtype, "sum")
+                ok = all(np.array_equal(to_host(t, dtype), exp) for t in ts)
+                bad += 0 if ok else 1
+                print(dtype, algo, proto, count, "ok" if ok else "MISMATCH", flush=True)
+os.environ["POLAR_TWOSHOT_TMA"] = "1"
+ct = L.Comm.virtual(n, 0)
+xs = synth.gen_ranks("f32", 70_001, n, cfg=6, dist="ints")
+ts = [to_device(x, "f32") for x in xs]
+ct.allreduce_forced(ts, "twoshot", "simple", 2)
+torch.cuda.synchronize()
+ok = all(np.array_equal(to_host(t, "f32"), orc.allreduce(xs, "f32", "sum")) for t in ts)
+bad += 0 if ok else 1
+print("tma twoshot", "ok" if ok else "MISMATCH", flush=True)
+sends = [torch.randn(n * 1000, device="cuda") for _ in range(n)]
+recvs = [torch.empty(1000, device="cuda") for _ in range(n)]
+c.reduce_scatter(sends, recvs)
+c.all_gather(recvs, sends)
+c.broadcast(sends, root=1)
+probe = c.p2p_probe([torch.zeros(4096, device="cuda") for _ in range(n)], iters=2)
+torch.cuda.synchronize()
+c.check()
+print("direct collectives + probe done", flush=True)
+ct.destroy()
+c.destroy()
+sys.exit(1 if bad else 0)
