@@ -19,9 +19,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2603_11438_b200", "libpolar.so")
 DT = {"i32": 2, "i64": 4, "f32": 7, "bf16": 9}
 ALGO = {0: "tree", 1: "ring", 3: "oneshot", 4: "twoshot"}
-PROTO = {0: "ll", 2: "simple"}
+PROTO = {0: "ll", 1: "ll128", 2: "simple"}
 OP = {0: "sum", 2: "max", 3: "min"}
-PATS = ["LDG.E.128", "STG.E.128", "STRONG.SYS", "STRONG.GPU", "UBLKCP.S.G", "UBLKCP.G.S", "SYNCS",
+PATS = ["LDG.E.128", "STG.E.128", "STRONG.SYS", "STRONG.GPU", "UBLKCP.S.G", "UBLKCP.G.S", "SYNCS", "SHFL", "VOTE",
         "MEMBAR.ALL.SYS", "MEMBAR.ALL.GPU", "FADD", "NANOSLEEP"]
 
 
