@@ -71,7 +71,7 @@ def main():
         for size in sizes:
             _, algo, proto, nch = best[size]
             code = (L.ALGO_CODES[algo], L.PROTO_CODES[proto], nch)
-            if rows and rows[-1][3:] == code:
+            if rows and tuple(rows[-1][3:]) == code:
                 rows[-1][2] = size
             else:
                 rows.append([0, n, size, *code])
