@@ -82,6 +82,35 @@ __device__ __forceinline__ void geo_slice(const Geo& g, unsigned long long NP, u
     if (hi > NP) hi = NP;
 }
 
+// Entry / exit handshakes of the zero-copy kernels (two-shot Simple, the direct
+// collectives): entry = every rank's input is ready; exit = no peer still reads
+// or writes my buffer.  A real comm needs both: its peers are other processes'
+// launches.  A virtual comm runs every rank in ONE grid, which starts after the
+// inputs' producers (stream order; griddepcontrol.wait under PDL) and whose
+// completion precedes any later use of the buffers, and the zero-copy kernels
+// have no other cross-rank dependency — so the launch subsumes both handshakes
+// and virtual comms skip them (POLAR_VIRTUAL_HANDSHAKE=1 builds keep them).
+#ifndef POLAR_VIRTUAL_HANDSHAKE
+#define POLAR_VIRTUAL_HANDSHAKE 0
+#endif
+__device__ __forceinline__ bool handshake_entry(const Params& P, const Who& w, uint64_t e) {
+    if (!P.sys && !POLAR_VIRTUAL_HANDSHAKE) return true;
+    if (w.tid < w.n) jitter(P), st_release(flag_ptr(P, w.tid, F_ENTRY, w.c, w.r), e, P.sys);
+    bool ok = true;
+    if (w.tid < w.n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, w.tid), e);
+    return __syncthreads_and(ok) != 0;
+}
+__device__ __forceinline__ bool handshake_exit(const Params& P, const Who& w, uint64_t e) {
+    if (!P.sys && !POLAR_VIRTUAL_HANDSHAKE) return true;
+    if (w.tid < w.n) {
+        fence_acq_rel(P.sys);
+        jitter(P), st_relaxed(flag_ptr(P, w.tid, F_EXIT, w.c, w.r), e, P.sys);
+    }
+    bool ok = true;
+    if (w.tid < w.n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, w.tid), e);
+    return __syncthreads_and(ok) != 0;
+}
+
 // ===================================================================== two-shot
 // Simple, zero-copy on symmetric buffers: entry barrier; owner r reads shard r
 // from every rank, reduces in rank order, stores the result into every rank's
@@ -319,10 +348,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e = st->epoch + 1;
     trace_point(P, 0);
-    if (tid < n) jitter(P), st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
-    bool ok = true;
-    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
-    if (!__syncthreads_and(ok)) return;
+    if (!handshake_entry(P, w, e)) return;
     trace_point(P, 1);
 
     // Owner r's shard [s0, s1) is processed by its nch CTAs with DYNAMIC chunk
@@ -342,13 +368,7 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     }
     __syncthreads();
     trace_point(P, 2);
-    if (tid < n) {
-        fence_acq_rel(P.sys);
-        jitter(P), st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
-    }
-    ok = true;
-    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
-    if (!__syncthreads_and(ok)) return;
+    if (!handshake_exit(P, w, e)) return;
     trace_point(P, 3);
     epoch_publish(P, w, e);
 }
@@ -1165,10 +1185,7 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) 
     const int n = w.n, tid = w.tid;
     ChanState* st = chan_state(P, w.r, w.c);
     const uint64_t e = st->epoch + 1;
-    if (tid < n) jitter(P), st_release(flag_ptr(P, tid, F_ENTRY, w.c, w.r), e, P.sys);
-    bool ok = true;
-    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, tid), e);
-    if (!__syncthreads_and(ok)) return;
+    if (!handshake_entry(P, w, e)) return;
     const unsigned long long NP = npacks<ES>(P);
     const size_t blk_bytes = (size_t)P.count * ES;
     unsigned long long a, b;
@@ -1220,13 +1237,7 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) 
             }
     }
     __syncthreads();
-    if (tid < n) {
-        fence_acq_rel(P.sys);
-        jitter(P), st_relaxed(flag_ptr(P, tid, F_EXIT, w.c, w.r), e, P.sys);
-    }
-    ok = true;
-    if (tid < n) ok = wait_geq(P, flag_ptr(P, w.r, F_EXIT, w.c, tid), e);
-    if (!__syncthreads_and(ok)) return;
+    if (!handshake_exit(P, w, e)) return;
     epoch_publish(P, w, e);
 }
 
