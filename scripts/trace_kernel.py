@@ -55,6 +55,10 @@ def main():
             "loop_end_us_min": round(float(t[:, 2].min()), 1), "loop_end_us_max": round(float(t[:, 2].max()), 1),
             "exit_wait_us_max": round(float((t[:, 3] - t[:, 2]).max()), 1),
             "nch": nch, "mib": a.mib,
+            # per rank (owner): earliest and latest loop end of its CTAs (virtual
+            # comms: block b = rank b / nch)
+            "owner_loop_end_us": [[round(float(t[r * nch:(r + 1) * nch, 2].min()), 1),
+                                   round(float(t[r * nch:(r + 1) * nch, 2].max()), 1)] for r in range(a.n)],
         }
         print(json.dumps(rep_), flush=True)
     # inter-kernel gap: two back-to-back launches traced into separate buffers
