@@ -314,3 +314,23 @@ def test_beyond_2pow31_elements(algo, proto):
     finally:
         del ts
         torch.cuda.empty_cache()
+
+
+def test_single_rank_is_identity_without_launch():
+    """n = 1 (SURVEY.md §8(c) reading 10): every call is an in-place identity,
+    decided (the decision is recorded) but not launched."""
+    c = L.Comm.virtual(1, 0)
+    try:
+        x = torch.arange(1000, dtype=torch.float32, device="cuda")
+        before = c.launches()
+        c.allreduce([x])
+        assert c.last_decision().as_tuple() == OP.decide([], 0, 1, 4000)
+        for algo in ALGOS:
+            for proto in PROTOS:
+                c.allreduce_forced([x], algo, proto, 4)
+        torch.cuda.synchronize()
+        c.check()
+        assert c.launches() == before
+        assert torch.equal(x, torch.arange(1000, dtype=torch.float32, device="cuda"))
+    finally:
+        c.destroy()
