@@ -365,6 +365,22 @@ def run_polar(args):
                      "pingpong_us_max": round(max(p["pingpong_us"] for p in probe), 2),
                      "what": "virtual ranks: every peer is local HBM; sums over the 8 concurrent ranks"}
 
+    if real:
+        # N > 1: the bound is the per-GPU NVLink path, not HBM.  Algorithmic bytes
+        # per launch = each rank's egress 2(n-1)/n S (RS + AG), so achieved = busBW;
+        # peak = the p2p probe's measured per-GPU load/store rate (min over ranks),
+        # else the nominal 900 GB/s per direction.
+        measured = min(probe_out["load_gbs_min_over_ranks"], probe_out["store_gbs_min_over_ranks"])
+        use_probe = not shared and measured > 0
+        npeak = round(measured, 1) if use_probe else 900.0
+        hbm_roof = roof
+        roof = {"bound": "nvlink", "achieved": round(value, 1), "peak": npeak, "unit": "GB/s",
+                "frac": round(value / npeak, 4), "traffic": None,
+                "peak_source": ("measured: p2p probe, min over ranks of peer load/store GB/s" if use_probe
+                                else "nominal 900 GB/s per direction per GPU (B200 NVLink 5)"),
+                "algorithmic_bytes_per_launch": int(S_BYTES * 2 * (n - 1) / n), "kernel": hbm_roof["kernel"],
+                "note": "per-rank NVLink egress; the local-HBM view is in 'hbm'", "hbm": hbm_roof}
+
     nccl = None
     if real and not shared:
         nccl = time_nccl(args, bufs[0], count, n, stream)

@@ -47,4 +47,5 @@ def test_bench_torchrun_two_ranks_shared_gpu():
     assert d["n_gpus"] == 2 and d["config"]["nranks"] == 2 and d["config"]["shared_gpu_test"]
     assert d["value"] > 0 and d["gpu_launches"] == 5
     assert d["decision"]["algo"] == "twoshot"
+    assert d["roofline"]["bound"] == "nvlink" and d["roofline"]["hbm"]["bound"] == "hbm"
     assert d["e2e"]["h2d_bytes_per_step"] == d["config"]["bytes_per_rank"]
