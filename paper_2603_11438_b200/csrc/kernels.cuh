@@ -127,12 +127,12 @@ struct TwoShotGeo {
     unsigned long long* work;
 };
 #ifndef POLAR_TS_BIG
-#define POLAR_TS_BIG 2048
+#define POLAR_TS_BIG 1024
 #endif
 #ifndef POLAR_TS_SMALL
 #define POLAR_TS_SMALL 512
 #endif
-constexpr unsigned long long kTsBig = POLAR_TS_BIG, kTsSmall = POLAR_TS_SMALL;   // packs (32 KiB / 8 KiB per buffer)
+constexpr unsigned long long kTsBig = POLAR_TS_BIG, kTsSmall = POLAR_TS_SMALL;   // packs (16 KiB / 8 KiB per buffer)
 
 template <int DT, int OP, int N>
 __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, const TwoShotGeo& g) {
