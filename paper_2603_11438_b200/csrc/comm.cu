@@ -257,9 +257,9 @@ polar_status alloc_common(polar_comm_s* c) {
         const char* ev = std::getenv("POLAR_PDL");
         c->pdl = !(ev && ev[0] == '0');
         // TMA-staged two-shot: POLAR_TWOSHOT_TMA=1 always, =0 never, unset = auto:
-        // virtual comms with n <= 2 and >= 64 MiB (the measured crossover: TMA 4.35
-        // vs LDG 4.13 TB/s at n=2/512 MiB; LDG ahead at n=8 and below 64 MiB, where
-        // the bulk pipeline fill costs ~8 us).  Real comms stay on LDG by default
+        // virtual comms with n <= 4 and >= 64 MiB (measured, bf16 busBW at 1 GiB:
+        // n=2 1103 vs 680, n=4 1247 vs 1170 GB/s; equal at n=8; LDG ahead below
+        // 64 MiB, where the bulk pipeline fill costs ~8 us).  Real comms stay on LDG by default
         // until bulk copies over peer-mapped NVLink memory are validated on a
         // multi-GPU box (they are tested over same-GPU CUDA-IPC mappings).
         c->jitter_ns = (unsigned)env_size("POLAR_JITTER_NS", 0);
@@ -490,7 +490,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         P.seq = ++c->tel_seq;
     }
     const bool ts_simple = d.algo == POLAR_ALGO_TWOSHOT && d.proto == POLAR_PROTO_SIMPLE;
-    const bool tma_auto = c->is_virtual && c->nranks <= 2 && count * (size_t)es >= (64u << 20);
+    const bool tma_auto = c->is_virtual && c->nranks <= 4 && count * (size_t)es >= (64u << 20);
     P.tma = (ts_simple && (c->tma_mode == 1 || (c->tma_mode == 2 && tma_auto))) ? 1 : 0;
     const size_t smem = P.tma ? dev::tma_smem_bytes(c->nranks) : 0;
     const size_t bytes = count * (size_t)es;

@@ -124,6 +124,7 @@ __device__ __forceinline__ bool handshake_exit(const Params& P, const Who& w, ui
 // out of the others' live ranges (the body-level switch spilled at 128 regs).
 struct TwoShotGeo {
     unsigned long long s0, s1, nbig, bigend, nchunks, nfull, wbase;
+    unsigned long long big, small;   // chunk sizes in packs
     unsigned long long* work;
 };
 #ifndef POLAR_TS_BIG
@@ -133,6 +134,9 @@ struct TwoShotGeo {
 #define POLAR_TS_SMALL 512
 #endif
 constexpr unsigned long long kTsBig = POLAR_TS_BIG, kTsSmall = POLAR_TS_SMALL;   // packs (16 KiB / 8 KiB per buffer)
+// the TMA pipeline restarts per grab, so it takes bigger chunks (32 KiB per buffer:
+// n = 2 at 1 GiB 906 -> 1098 GB/s busBW vs 16 KiB)
+constexpr unsigned long long kTsBigTma = 2048;
 
 template <int DT, int OP, int N>
 __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, const TwoShotGeo& g) {
@@ -154,8 +158,8 @@ __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, cons
     while (k < g.nchunks) {
         __syncthreads();                                         // everyone has read s_next
         if (tid == 0) s_next = atomicAdd(g.work, 1ull) - g.wbase;   // prefetch the next grab
-        const unsigned long long a = g.s0 + (k < g.nbig ? k * kTsBig : g.bigend + (k - g.nbig) * kTsSmall);
-        unsigned long long b = a + (k < g.nbig ? kTsBig : kTsSmall);
+        const unsigned long long a = g.s0 + (k < g.nbig ? k * g.big : g.bigend + (k - g.nbig) * g.small);
+        unsigned long long b = a + (k < g.nbig ? g.big : g.small);
         if (b > g.s1) b = g.s1;
         if (b <= g.nfull) {
             // fast path: full, 16-B aligned packs
@@ -264,8 +268,8 @@ __device__ void twoshot_tma(const Params& P, const Who& w, const TwoShotGeo& g) 
                 while (!done && pos >= fend) {
                     const unsigned long long k = atomicAdd(g.work, 1ull) - g.wbase;
                     if (k >= g.nchunks) { done = true; break; }
-                    const unsigned long long a = g.s0 + (k < g.nbig ? k * kTsBig : g.bigend + (k - g.nbig) * kTsSmall);
-                    unsigned long long b = a + (k < g.nbig ? kTsBig : kTsSmall);
+                    const unsigned long long a = g.s0 + (k < g.nbig ? k * g.big : g.bigend + (k - g.nbig) * g.small);
+                    unsigned long long b = a + (k < g.nbig ? g.big : g.small);
                     if (b > g.s1) b = g.s1;
                     pos = a;
                     fend = b < g.nfull ? b : (a > g.nfull ? a : g.nfull);
@@ -325,16 +329,19 @@ __device__ void twoshot_tma(const Params& P, const Who& w, const TwoShotGeo& g) 
 }
 
 // owner j's shard of the zero-copy two-shot as a chunk queue: big chunks first,
-// then small ones for the last nch * kTsBig packs (balanced tail)
+// then small ones for the last nch * big packs (balanced tail)
 template <int ES>
-__device__ __forceinline__ TwoShotGeo twoshot_geo(const Params& P, int j, uint64_t e) {
+__device__ __forceinline__ TwoShotGeo twoshot_geo(const Params& P, int j, uint64_t e, unsigned long long big,
+                                                  unsigned long long small) {
     TwoShotGeo g;
+    g.big = big;
+    g.small = small;
     split_range(0, npacks<ES>(P), P.nranks, j, g.s0, g.s1);
     const unsigned long long L = g.s1 - g.s0;
-    const unsigned long long tail = L < (unsigned long long)P.nch * kTsBig ? L : (unsigned long long)P.nch * kTsBig;
-    g.nbig = (L - tail) / kTsBig;
-    g.bigend = g.nbig * kTsBig;
-    g.nchunks = g.nbig + (L - g.bigend + kTsSmall - 1) / kTsSmall;
+    const unsigned long long tail = L < (unsigned long long)P.nch * big ? L : (unsigned long long)P.nch * big;
+    g.nbig = (L - tail) / big;
+    g.bigend = g.nbig * big;
+    g.nchunks = g.nbig + (L - g.bigend + small - 1) / small;
     g.nfull = P.vec ? (P.count / (16 / ES)) : 0;   // packs safe for the fast path
     g.work = reinterpret_cast<unsigned long long*>(&chan_state(P, j, 0)->work);
     g.wbase = (unsigned long long)e << 32;
@@ -357,8 +364,9 @@ __device__ void twoshot_simple(const Params& P, const Who& w) {
     // SM takes fewer chunks (static slices left a ~15 % loop-time spread,
     // measured with polar_comm_set_trace).  Big chunks first, then small ones
     // for the last nch*kTsBig packs so the tail is balanced too.
-    const TwoShotGeo g = twoshot_geo<ES>(P, w.r, e);
-    if (P.tma && P.vec) {
+    const bool tma = P.tma && P.vec;
+    const TwoShotGeo g = twoshot_geo<ES>(P, w.r, e, tma ? kTsBigTma : kTsBig, kTsSmall);
+    if (tma) {
         twoshot_tma<DT, OP>(P, w, g);
     } else switch (n) {
         case 2: twoshot_loop<DT, OP, 2>(P, w, g); break;
