@@ -376,8 +376,9 @@ struct BootRec {
     uint32_t nranks, rank;
     uint64_t layout_hash;
     uint64_t pad;
+    unsigned char uuid[16];   // the rank's GPU (zeros from polar_bootstrap_check)
 };
-static_assert(sizeof(BootRec) == 32, "bootstrap record is 32 B");
+static_assert(sizeof(BootRec) == 48, "bootstrap record is 48 B");
 constexpr uint64_t kBootMagic = 0x706f6c6172763031ull;   // "polarv01"
 
 uint64_t layout_hash(const Layout& L) {
@@ -388,16 +389,23 @@ uint64_t layout_hash(const Layout& L) {
     return h;
 }
 
-polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgather_fn ag, void* user) {
-    BootRec mine{kBootMagic, (uint32_t)nranks, (uint32_t)rank, layout_hash(L), 0};
+// uuid: this rank's GPU (may be null); *shared_gpu (may be null) is set when
+// another rank reports the same GPU (several ranks on one device, e.g. MPS).
+polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgather_fn ag, void* user,
+                             const unsigned char* uuid = nullptr, bool* shared_gpu = nullptr) {
+    BootRec mine{kBootMagic, (uint32_t)nranks, (uint32_t)rank, layout_hash(L), 0, {}};
+    if (uuid) std::memcpy(mine.uuid, uuid, sizeof(mine.uuid));
     std::vector<BootRec> all(nranks);
     if (ag(&mine, all.data(), sizeof(BootRec), user) != 0) return POLAR_ESTATE;
+    bool shared = false;
     for (int p = 0; p < nranks; ++p) {
         const BootRec& r = all[p];
         if (r.magic != kBootMagic || r.nranks != (uint32_t)nranks || r.rank != (uint32_t)p ||
             r.layout_hash != mine.layout_hash)
             return POLAR_ESTATE;
+        if (p != rank && std::memcmp(r.uuid, mine.uuid, sizeof(mine.uuid)) == 0) shared = true;
     }
+    if (shared_gpu) *shared_gpu = shared;
     return POLAR_OK;
 }
 
@@ -644,7 +652,18 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     if (st == POLAR_OK) st = cuerr(cudaMalloc(reinterpret_cast<void**>(&c->scratch_own[0]), c->L.total));
     if (st == POLAR_OK) st = cuerr(cudaMemset(c->scratch_own[0], 0, c->L.total));
     if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
-    if (st == POLAR_OK) st = bootstrap_check(nranks, rank, c->L, ag, user);
+    cudaDeviceProp prop{};
+    if (st == POLAR_OK) st = cuerr(cudaGetDeviceProperties(&prop, cuda_device));
+    bool shared_gpu = false;
+    if (st == POLAR_OK)
+        st = bootstrap_check(nranks, rank, c->L, ag, user, reinterpret_cast<const unsigned char*>(prop.uuid.bytes),
+                             &shared_gpu);
+    // Ranks sharing one GPU (MPS) must not use programmatic dependent launch: a
+    // rank's pre-launched next kernels can hold the SMs another rank's CURRENT
+    // kernel needs, and the cross-rank waits then never complete (measured: 4
+    // processes under MPS time out with PDL, run without).  One rank per GPU is
+    // safe: a rank's own current kernel is always fully resident first.
+    if (shared_gpu) c->pdl = false;
     if (st == POLAR_OK) st = exchange_and_map(c, c->scratch_own[0], c->scratch);
     if (st == POLAR_OK) st = init_barrier(c);
     if (st != POLAR_OK) { destroy_comm(c, false); return st; }
