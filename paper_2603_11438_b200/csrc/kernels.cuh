@@ -958,12 +958,10 @@ __device__ void ring(const Params& P, const Who& w) {
             if (s == n - 1) k = (r + 1) % n;
             const unsigned long long ks = base + L * (unsigned long long)k / n;
             const unsigned long long ke = base + L * (unsigned long long)(k + 1) / n;
-            // ---- waits (one thread), then barrier
+            // ---- waits (thread 0: the fill from prev, thread 1: the credit from next), then barrier
             bool ok = true;
-            if (tid == 0) {
-                if (do_recv && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, tail_in, recvd + 1);
-                if (ok && do_send && sent >= (unsigned long long)kSteps) ok = wait_geq(P, head_in, sent - kSteps + 1);
-            }
+            if (tid == 0 && do_recv && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, tail_in, recvd + 1);
+            if (tid == 1 && do_send && sent >= (unsigned long long)kSteps) ok = wait_geq(P, head_in, sent - kSteps + 1);
             if (!__syncthreads_and(ok)) return;
             const uint4* src = ring_slot<PROTO>(P, r, c, recvd);
             uint4* dst = ring_slot<PROTO>(P, next, c, sent);
@@ -1159,12 +1157,10 @@ __device__ void tree(const Params& P, const Who& w) {
     for (unsigned long long s = 0; s < nslots; ++s) {
         const unsigned long long lo = ca + s * SP, hi = (lo + SP < cb) ? lo + SP : cb;
         bool ok = true;
-        if (tid == 0) {
-            if (!root && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), drecv + 1);
-            if (dsent >= (unsigned long long)kSteps)
-                for (int k = 0; k < nchild && ok; ++k)
-                    ok = wait_geq(P, flag_ptr(P, r, F_TREE_DHEAD, c, k), dsent - kSteps + 1);
-        }
+        // thread 0: the parent's fill; threads 1, 2: the children's credits
+        if (tid == 0 && !root && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), drecv + 1);
+        if (tid >= 1 && tid <= nchild && dsent >= (unsigned long long)kSteps)
+            ok = wait_geq(P, flag_ptr(P, r, F_TREE_DHEAD, c, tid - 1), dsent - kSteps + 1);
         if (!__syncthreads_and(ok)) return;
         const uint4* src = root ? nullptr : tree_dn_slot<PROTO>(P, r, c, drecv);
         const uint64_t fin = drecv + 1, fout = dsent + 1;
