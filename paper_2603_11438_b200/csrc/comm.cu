@@ -58,7 +58,7 @@ Layout make_layout(bool with_bounce) {
     L.os_off = off; off = align_up(off + 2 * kMaxRanks * L.os_chunk, 4096);
     L.osll_chunk = align_up(env_size("POLAR_OSLL_CHUNK", 256 << 10), 512);
     L.osll_off = off; off = align_up(off + 2 * kMaxRanks * 2 * L.osll_chunk, 4096);
-    L.tsll_chunk = align_up(env_size("POLAR_TSLL_CHUNK", 64 << 10), 512);
+    L.tsll_chunk = align_up(env_size("POLAR_TSLL_CHUNK", 256 << 10), 512);
     L.tsll_off = off; off = align_up(off + 2 * (2 * kMaxRanks * 2 * L.tsll_chunk), 4096);
     L.ring_slot = align_up(env_size("POLAR_RING_SLOT", 128 << 10), 512);
     L.ring_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring_slot, 4096);

@@ -102,6 +102,29 @@ __device__ __forceinline__ void st_plain(uint4* p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+// Consumed Simple staging / FIFO data: drop its L2 lines without write-back
+// (`discard.global.L2`).  The bytes were written by a peer, read once, and will be
+// overwritten before they are read again (the next lap of the FIFO / the next
+// call), so writing the dirty lines back to HBM is wasted bandwidth.  The slot's
+// contents become undefined, which Simple tolerates: a fill flag published after
+// the next write, never the data itself, says when a slot is valid.  The whole
+// CTA calls this after a barrier that ends every read of [p, p + bytes); p is
+// 128-B aligned, and the last partial line is dropped too (its tail is unused).
+// Off by default: measured on 8 virtual ranks (profiles/r01_discard_ab.jsonl) the
+// ring's DRAM traffic falls to ~2.1 n S and 128 MiB runs 948 -> 887 us, but the
+// extra barrier per step costs more everywhere else (ring 1 MiB 38.7 -> 42.0 us,
+// tree 128 MiB 1269 -> 1346 us, one-shot 8 MiB 164 -> 177 us).
+#ifndef POLAR_DISCARD
+#define POLAR_DISCARD 0
+#endif
+__device__ __forceinline__ void discard_l2(const void* p, unsigned long long bytes) {
+#if POLAR_DISCARD
+    const char* c = static_cast<const char*>(p);
+    for (unsigned long long o = (unsigned long long)threadIdx.x * 128; o < bytes; o += (unsigned long long)blockDim.x * 128)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(c + o) : "memory");
+#endif
+}
+
 // LL line: 16 B = {d0, flag, d1, flag}; written with one 16-B volatile store,
 // polled with one 16-B volatile load.
 __device__ __forceinline__ void st_ll(uint4* p, uint32_t d0, uint32_t d1, uint32_t flag) {

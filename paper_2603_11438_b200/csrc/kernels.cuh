@@ -133,6 +133,9 @@ struct TwoShotGeo {
 #ifndef POLAR_TS_SMALL
 #define POLAR_TS_SMALL 512
 #endif
+#ifndef POLAR_TS_UGEN
+#define POLAR_TS_UGEN 1   // packs per thread per rank in flight on the generic (n >= 5) path
+#endif
 constexpr unsigned long long kTsBig = POLAR_TS_BIG, kTsSmall = POLAR_TS_SMALL;   // packs (16 KiB / 8 KiB per buffer)
 // the TMA pipeline restarts per grab, so it takes bigger chunks (32 KiB per buffer:
 // n = 2 at 1 GiB 906 -> 1098 GB/s busBW vs 16 KiB)
@@ -142,7 +145,7 @@ template <int DT, int OP, int N>
 __device__ __forceinline__ void twoshot_loop(const Params& P, const Who& w, const TwoShotGeo& g) {
     constexpr int ES = DType<DT>::ES;
     constexpr int NR = N ? N : kMaxRanks;
-    constexpr int U = (N >= 2 && N <= 4) ? 8 / N : 1;
+    constexpr int U = (N >= 2 && N <= 4) ? 8 / N : POLAR_TS_UGEN;
     const int n = w.n, tid = w.tid;
     __shared__ unsigned long long s_next;
     if (tid == 0) {
@@ -839,6 +842,13 @@ __device__ void oneshot_simple(const Params& P, const Who& w) {
                 if (p < n) acc_add<DT, OP>(acc, v[p]);
             store_pack<ES>(P, mine, i, acc_fin<DT>(acc));
         }
+        if (POLAR_DISCARD) {
+            // staging consumed; the peers refill this parity only after our next
+            // chunk's (or call's) flag, which the next barrier + fence orders after this
+            __syncthreads();
+            for (int p = 0; p < n; ++p)
+                if (p != w.r) discard_l2(os_slot(P, w.r, par, p) + off, (hi - lo) * 16ull);
+        }
     }
     epoch_publish(P, w, e0 + g.nchunks);
 }
@@ -1010,11 +1020,14 @@ __device__ void ring(const Params& P, const Who& w) {
                 return true;
             });
             if (!__syncthreads_and(ok)) return;
+            if (PROTO == POLAR_PROTO_SIMPLE && POLAR_DISCARD && do_recv) {
+                // the slot is consumed: drop its lines before the credit frees it
+                discard_l2(src, (ke - ks) * (unsigned long long)(s < n ? AW : 1) * 16ull);
+                __syncthreads();
+            }
             if (tid == 0) {
-                if (do_send && PROTO == POLAR_PROTO_SIMPLE) {
-                    fence_acq_rel(P.sys);
-                    jitter(P), st_relaxed(tail_out, sent + 1, P.sys);
-                }
+                if (PROTO == POLAR_PROTO_SIMPLE && (do_send || (POLAR_DISCARD && do_recv))) fence_acq_rel(P.sys);
+                if (do_send && PROTO == POLAR_PROTO_SIMPLE) jitter(P), st_relaxed(tail_out, sent + 1, P.sys);
                 if (do_recv) jitter(P), st_relaxed(head_out, recvd + 1, P.sys);
             }
             if (do_send) ++sent;
@@ -1143,11 +1156,15 @@ __device__ void tree(const Params& P, const Who& w) {
             return true;
         });
         if (!__syncthreads_and(ok)) return;
+        if (PROTO == POLAR_PROTO_SIMPLE && POLAR_DISCARD && nchild) {
+            for (int k = 0; k < nchild; ++k)
+                discard_l2(tree_up_slot<PROTO>(P, r, c, k, urecv[k]), (hi - lo) * (unsigned long long)AW * 16ull);
+            __syncthreads();
+        }
         if (tid == 0) {
-            if (!root && PROTO == POLAR_PROTO_SIMPLE) {
-                fence_acq_rel(P.sys);
+            if (PROTO == POLAR_PROTO_SIMPLE && (!root || (POLAR_DISCARD && nchild))) fence_acq_rel(P.sys);
+            if (!root && PROTO == POLAR_PROTO_SIMPLE)
                 jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1, P.sys);
-            }
             for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1, P.sys);
         }
         if (!root) ++usent;
@@ -1184,11 +1201,14 @@ __device__ void tree(const Params& P, const Who& w) {
             return true;
         });
         if (!__syncthreads_and(ok)) return;
+        if (PROTO == POLAR_PROTO_SIMPLE && POLAR_DISCARD && !root) {
+            discard_l2(src, (hi - lo) * 16ull);
+            __syncthreads();
+        }
         if (tid == 0) {
-            if (PROTO == POLAR_PROTO_SIMPLE && nchild) {
-                fence_acq_rel(P.sys);
+            if (PROTO == POLAR_PROTO_SIMPLE && (nchild || (POLAR_DISCARD && !root))) fence_acq_rel(P.sys);
+            if (PROTO == POLAR_PROTO_SIMPLE && nchild)
                 for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1, P.sys);
-            }
             if (!root) jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1, P.sys);
         }
         if (nchild) ++dsent;
