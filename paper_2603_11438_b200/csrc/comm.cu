@@ -60,7 +60,7 @@ Layout make_layout(bool with_bounce) {
     L.osll_off = off; off = align_up(off + 2 * kMaxRanks * 2 * L.osll_chunk, 4096);
     L.tsll_chunk = align_up(env_size("POLAR_TSLL_CHUNK", 256 << 10), 512);
     L.tsll_off = off; off = align_up(off + 2 * (2 * kMaxRanks * 2 * L.tsll_chunk), 4096);
-    L.ring_slot = align_up(env_size("POLAR_RING_SLOT", 128 << 10), 512);
+    L.ring_slot = align_up(env_size("POLAR_RING_SLOT", 120 << 10), 512);   // 7680 f32 packs: whole 480-thread x 4-pack batches per half slot (ring_simple_ws)
     L.ring_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring_slot, 4096);
     L.ringll_slot = align_up(env_size("POLAR_RINGLL_SLOT", 64 << 10), 512);
     L.ringll_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ringll_slot, 4096);

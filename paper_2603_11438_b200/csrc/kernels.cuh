@@ -1040,6 +1040,194 @@ __device__ void ring(const Params& P, const Who& w) {
     }
 }
 
+// Ring Simple, warp specialised (POLAR_RING_WS).  Measured on the plain ring
+// above: every step's synchronisation point (barrier, fence, tail flag, the
+// successor's poll) costs ~1.8 us of L2 round trips even when nothing waits, and
+// the ring runs in lock-step, so each step pays it on top of its data time
+// (DESIGN.md "Ring on virtual ranks").  Here warp 0 is a synchronisation warp
+// and warps 1.. move data:
+//   * the slot travels in RQ sub-slices (units), each published by its own tail
+//     value (sent * RQ + q + 1), so a successor starts a step while its producer
+//     is still filling the step's later sub-slices;
+//   * the sync warp polls unit g's fill flag (and, at a step's first unit, the
+//     credit) and hands the unit to the data warps with bar.arrive READY[g&1];
+//     it then waits DONE[(g-1)&1] and publishes unit g-1 (fence, tail; the
+//     credit after a step's last unit) — polls and fences run while the data
+//     warps already move unit g;
+//   * data warps: bar.sync READY[g&1], move the unit, bar.arrive DONE[g&1].
+// Two barrier ids per direction suffice: the sync warp arrives READY for unit g
+// only after DONE of unit g-2 completed (so every data warp passed READY of
+// g-2), and data warps arrive DONE for g+2 only after READY of g+2, which the sync
+// warp arrives after it consumed DONE of g.  Only the sync warp spins; on a
+// timeout it raises s_abort before its arrive and leaves, and the data warps leave
+// at the next READY.
+#ifndef POLAR_RING_WS
+#define POLAR_RING_WS 1
+#endif
+#ifndef POLAR_RING_WS_SUB
+#define POLAR_RING_WS_SUB 2
+#endif
+__device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+
+template <int DT, int OP>
+__device__ void ring_simple_ws(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int AW = AccWords<DT>::N;
+    constexpr int U = POLAR_BATCH_SIMPLE / AW > 0 ? POLAR_BATCH_SIMPLE / AW : 1;
+    constexpr int RQ = POLAR_RING_WS_SUB;
+    // unit g's fill was published by the predecessor at ITS unit g - RQ, and a
+    // rank publishes unit g - 1 only after its waits for unit g: RQ = 1 would make
+    // every rank wait for its predecessor's wait around the ring (measured: timeout)
+    static_assert(RQ >= 2, "the publication lag needs >= 2 sub-slices per slot");
+    constexpr int kReady = 1, kDone = 3;          // named barrier ids (0 is __syncthreads)
+    using W = Wire<POLAR_PROTO_SIMPLE>;
+    const int n = w.n, tid = w.tid, r = w.r, c = w.c;
+    const int next = (r + 1) % n, prev = (r + n - 1) % n;
+    const int nthr = blockDim.x;
+    ChanState* st = chan_state(P, r, c);
+    unsigned long long sent = st->ring_sent, recvd = st->ring_recv;
+    const unsigned long long SP = W::units(P.ring_slot) / AW;   // element packs per slot
+    const unsigned long long NP = npacks<ES>(P);
+    unsigned long long ca, cb;
+    split_range(0, NP, P.nch, c, ca, cb);
+    char* mine = P.bufs[r];
+    const unsigned long long LC = SP * (unsigned long long)n;
+    __shared__ int s_abort;
+    if (tid == 0) s_abort = 0;
+    __syncthreads();
+
+    if (tid < 32) {
+        // ---------------------------------------------------------- sync warp
+        const int lane = tid;
+        uint64_t* head_in = flag_ptr(P, r, F_RING_HEAD, c, 0);    // credits from next
+        uint64_t* tail_in = flag_ptr(P, r, F_RING_TAIL, c, 0);    // fills from prev
+        uint64_t* tail_out = flag_ptr(P, next, F_RING_TAIL, c, 0);
+        uint64_t* head_out = flag_ptr(P, prev, F_RING_HEAD, c, 0);
+        unsigned long long g = 0;
+        uint64_t pub_tail = 0, pub_head = 0;              // unit g-1's flag values (0: none)
+        auto publish = [&]() {
+            nbar_sync(kDone + (int)((g - 1) & 1), nthr);  // unit g-1 moved by every data warp
+            if (lane == 0) {
+                fence_acq_rel(P.sys);
+                if (pub_tail) jitter(P), st_relaxed(tail_out, pub_tail, P.sys);
+                if (pub_head) jitter(P), st_relaxed(head_out, pub_head, P.sys);
+            }
+        };
+        for (unsigned long long base = ca; base < cb; base += LC) {
+            for (int s = 0; s < 2 * (n - 1) + 1; ++s) {
+                const bool do_recv = s > 0, do_send = s < 2 * (n - 1);
+                for (int q = 0; q < RQ; ++q) {
+                    int ok = 1;
+                    if (lane == 0) {
+                        if (do_recv) ok = wait_geq(P, tail_in, recvd * RQ + q + 1);
+                        if (ok && q == 0 && do_send && sent >= (unsigned long long)kSteps)
+                            ok = wait_geq(P, head_in, sent - kSteps + 1);
+                        if (!ok) *(volatile int*)&s_abort = 1;
+                    }
+                    ok = __shfl_sync(0xffffffffu, ok, 0);
+                    nbar_arrive(kReady + (int)(g & 1), nthr);
+                    if (!ok) return;
+                    if (g > 0) publish();
+                    pub_tail = do_send ? sent * RQ + q + 1 : 0;
+                    pub_head = (do_recv && q == RQ - 1) ? recvd + 1 : 0;
+                    ++g;
+                }
+                if (do_send) ++sent;
+                if (do_recv) ++recvd;
+            }
+        }
+        if (g > 0) publish();
+        if (lane == 0) {
+            st->ring_sent = sent;
+            st->ring_recv = recvd;
+        }
+        return;
+    }
+    // -------------------------------------------------------------- data warps
+    const unsigned long long D = (unsigned long long)(nthr - 32), dt = (unsigned long long)(tid - 32);
+    unsigned long long g = 0;
+    for (unsigned long long base = ca; base < cb; base += LC) {
+        const unsigned long long L = (cb - base < LC) ? cb - base : LC;
+        for (int s = 0; s < 2 * (n - 1) + 1; ++s) {
+            const bool do_send = s < 2 * (n - 1);
+            int k;
+            if (s < n) k = ((r - s) % n + n) % n;
+            else k = ((r - (s - n)) % n + n) % n;
+            if (s == n - 1) k = (r + 1) % n;
+            const unsigned long long ks = base + L * (unsigned long long)k / n;
+            const unsigned long long ke = base + L * (unsigned long long)(k + 1) / n;
+            const uint4* src = ring_slot<POLAR_PROTO_SIMPLE>(P, r, c, recvd);
+            uint4* dst = ring_slot<POLAR_PROTO_SIMPLE>(P, next, c, sent);
+            for (int q = 0; q < RQ; ++q) {
+                const unsigned long long qs = ks + (ke - ks) * (unsigned long long)q / RQ;
+                const unsigned long long qe = ks + (ke - ks) * (unsigned long long)(q + 1) / RQ;
+                nbar_sync(kReady + (int)(g & 1), nthr);
+                if (*(volatile int*)&s_abort) return;
+                for (unsigned long long i0 = qs + dt; i0 < qe; i0 += U * D) {
+                    Batch<U> b;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        b.i[u] = i0 + u * D;
+                        b.j[u] = b.i[u] - ks;               // wire index in the slot
+                        b.in[u] = b.act[u] = b.i[u] < qe;
+                    }
+                    uint4 own[U];
+                    if (s < n) load_batch<ES>(P, mine, b, own);
+                    if (s == 0) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (!b.in[u]) continue;
+                            Acc<DT> acc;
+                            acc_init<DT>(acc, own[u]);
+#pragma unroll
+                            for (int x = 0; x < AW; ++x) W::put(P, dst, b.j[u] * AW + x, acc.w[x], 0);
+                        }
+                    } else if (s < n) {
+                        uint4 in[U][AW];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int x = 0; x < AW; ++x)
+                                if (b.in[u]) in[u][x] = ld_cg(src + b.j[u] * AW + x);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (!b.in[u]) continue;
+                            Acc<DT> acc;
+#pragma unroll
+                            for (int x = 0; x < AW; ++x) acc.w[x] = in[u][x];
+                            acc_add<DT, OP>(acc, own[u]);
+                            if (s < n - 1) {
+#pragma unroll
+                                for (int x = 0; x < AW; ++x) W::put(P, dst, b.j[u] * AW + x, acc.w[x], 0);
+                            } else {
+                                const uint4 out = acc_fin<DT>(acc);
+                                store_pack<ES>(P, mine, b.i[u], out);
+                                W::put(P, dst, b.j[u], out, 0);
+                            }
+                        }
+                    } else {
+                        uint4 v[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (b.in[u]) v[u] = ld_cg(src + b.j[u]);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (!b.in[u]) continue;
+                            store_pack<ES>(P, mine, b.i[u], v[u]);
+                            if (do_send) W::put(P, dst, b.j[u], v[u], 0);
+                        }
+                    }
+                }
+                nbar_arrive(kDone + (int)(g & 1), nthr);
+                ++g;
+            }
+            if (do_send) ++sent;
+            if (s > 0) ++recvd;
+        }
+    }
+}
+
 // ======================================================================= tree
 // Binary tree per channel over positions pos = (rank - c) mod n (root = rank c
 // mod n); children 2pos+1, 2pos+2.  Up phase: node = own (op) child0 (op)
@@ -1244,7 +1432,8 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) oneshot_simple<DT, OP>(P, w);
         else oneshot_ll<DT, OP, PROTO>(P, w);
     } else if constexpr (ALGO == POLAR_ALGO_RING) {
-        ring<DT, OP, PROTO>(P, w);
+        if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_RING_WS) ring_simple_ws<DT, OP>(P, w);
+        else ring<DT, OP, PROTO>(P, w);
     } else {
         tree<DT, OP, PROTO>(P, w);
     }
