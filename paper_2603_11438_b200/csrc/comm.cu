@@ -64,7 +64,7 @@ Layout make_layout(bool with_bounce) {
     L.ring_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring_slot, 4096);
     L.ringll_slot = align_up(env_size("POLAR_RINGLL_SLOT", 64 << 10), 512);
     L.ringll_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ringll_slot, 4096);
-    L.tree_slot = align_up(env_size("POLAR_TREE_SLOT", 128 << 10), 512);
+    L.tree_slot = align_up(env_size("POLAR_TREE_SLOT", 120 << 10), 512);   // whole 480-thread batches per half slot (tree_simple_ws)
     L.tree_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.tree_slot, 4096);
     L.treell_slot = align_up(env_size("POLAR_TREELL_SLOT", 64 << 10), 512);
     L.treell_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.treell_slot, 4096);

@@ -1067,6 +1067,9 @@ __device__ void ring(const Params& P, const Who& w) {
 #ifndef POLAR_RING_WS_SUB
 #define POLAR_RING_WS_SUB 2
 #endif
+#ifndef POLAR_RING_WS_BATCH
+#define POLAR_RING_WS_BATCH POLAR_BATCH_SIMPLE   // packs per data thread per iteration (f32)
+#endif
 __device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 
@@ -1074,7 +1077,7 @@ template <int DT, int OP>
 __device__ void ring_simple_ws(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
     constexpr int AW = AccWords<DT>::N;
-    constexpr int U = POLAR_BATCH_SIMPLE / AW > 0 ? POLAR_BATCH_SIMPLE / AW : 1;
+    constexpr int U = POLAR_RING_WS_BATCH / AW > 0 ? POLAR_RING_WS_BATCH / AW : 1;
     constexpr int RQ = POLAR_RING_WS_SUB;
     // unit g's fill was published by the predecessor at ITS unit g - RQ, and a
     // rank publishes unit g - 1 only after its waits for unit g: RQ = 1 would make
@@ -1411,6 +1414,236 @@ __device__ void tree(const Params& P, const Who& w) {
     }
 }
 
+// Tree Simple, warp specialised (POLAR_TREE_WS): the ring's scheme
+// (ring_simple_ws) applied to both tree phases.  Units = half or whole slots; the sync
+// warp's lanes 0..2 poll the unit's fills (children up / parent down) and
+// credits (parent up / children down) in parallel, hand the unit over with
+// READY, and publish the previous unit (fence, tails, credits after a slot's
+// last unit) once its DONE completes.  At the up -> down boundary the last up
+// unit is published BEFORE the first down wait: the parent's down phase needs it.
+#ifndef POLAR_TREE_WS
+#define POLAR_TREE_WS 1
+#endif
+
+template <int DT, int OP, int RQ>
+__device__ void tree_simple_ws_impl(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int AW = AccWords<DT>::N;
+    constexpr int U = POLAR_RING_WS_BATCH / AW > 0 ? POLAR_RING_WS_BATCH / AW : 1;
+    constexpr int kReady = 1, kDone = 3;
+    using W = Wire<POLAR_PROTO_SIMPLE>;
+    const int n = w.n, tid = w.tid, r = w.r, c = w.c;
+    const int nthr = blockDim.x;
+    const int pos = ((r - c) % n + n) % n;
+    auto rank_of = [&](int q) { return (q + c) % n; };
+    const bool root = pos == 0;
+    const int parent = root ? -1 : rank_of((pos - 1) / 2);
+    const int my_child_idx = root ? 0 : (pos - 1) % 2;
+    int child[2] = {-1, -1};
+    int nchild = 0;
+    for (int k = 0; k < 2; ++k)
+        if (2 * pos + 1 + k < n) { child[k] = rank_of(2 * pos + 1 + k); nchild = k + 1; }
+    ChanState* st = chan_state(P, r, c);
+    unsigned long long usent = st->tree_usent, dsent = st->tree_dsent, drecv = st->tree_drecv;
+    unsigned long long urecv[2] = {st->tree_urecv[0], st->tree_urecv[1]};
+    const unsigned long long SP = W::units(P.tree_slot) / AW;   // element packs per slot
+    const unsigned long long NP = npacks<ES>(P);
+    unsigned long long ca, cb;
+    split_range(0, NP, P.nch, c, ca, cb);
+    const unsigned long long nslots = (cb - ca + SP - 1) / SP;
+    // Units per slot (RQ, chosen by tree_simple_ws).  The tree is acyclic (a child's publication never waits on
+    // its parent's current unit), so whole slots (RQ = 1) are valid here, unlike
+    // in the ring.  Measured (profiles/r01_tree_ws_ab.jsonl): half slots pipeline
+    // the levels when a channel has few slots (1 MiB 35.3 -> 29.7 us), whole slots
+    // win at many slots (128 MiB 1176 -> 1066 us) and for tiny messages (4 KiB
+    // 22.3 -> 19.0 us: fewer hand-offs).  Tail values count HALF slots whatever
+    // RQ is, so flags stay monotone across calls that choose differently.
+    constexpr unsigned long long QS = 2 / RQ;   // half slots per unit
+    char* mine = P.bufs[r];
+    __shared__ int s_abort;
+    if (tid == 0) s_abort = 0;
+    __syncthreads();
+
+    if (tid < 32) {
+        // ---------------------------------------------------------- sync warp
+        const int lane = tid;
+        unsigned long long g = 0;
+        bool pending = false;
+        uint64_t* pub_ptr[3] = {nullptr, nullptr, nullptr};   // unit g-1's flag stores
+        uint64_t pub_val[3] = {0, 0, 0};
+        int npub = 0;
+        auto publish = [&]() {
+            nbar_sync(kDone + (int)((g - 1) & 1), nthr);
+            if (lane == 0) {
+                fence_acq_rel(P.sys);
+                for (int x = 0; x < npub; ++x) jitter(P), st_relaxed(pub_ptr[x], pub_val[x], P.sys);
+            }
+            pending = false;
+        };
+        for (int phase = 0; phase < 2; ++phase) {
+            if (phase == 1 && pending) publish();   // the parent's down phase needs our last up unit
+            for (unsigned long long sl = 0; sl < nslots; ++sl) {
+                for (int q = 0; q < RQ; ++q) {
+                    // lanes 0, 1: fills (up: child k; down: lane 0 the parent);
+                    // lane 2 (up) / lanes 1, 2 (down): credits
+                    int ok = 1;
+                    if (phase == 0) {
+                        if (lane < nchild) ok = wait_geq(P, flag_ptr(P, r, F_TREE_UTAIL, c, lane), urecv[lane] * 2 + (q + 1) * QS);
+                        if (lane == 2 && q == 0 && !root && usent >= (unsigned long long)kSteps)
+                            ok = wait_geq(P, flag_ptr(P, r, F_TREE_UHEAD, c, 0), usent - kSteps + 1);
+                    } else {
+                        if (lane == 0 && !root) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), drecv * 2 + (q + 1) * QS);
+                        if (lane >= 1 && lane <= nchild && q == 0 && dsent >= (unsigned long long)kSteps)
+                            ok = wait_geq(P, flag_ptr(P, r, F_TREE_DHEAD, c, lane - 1), dsent - kSteps + 1);
+                    }
+                    ok = __all_sync(0xffffffffu, ok);
+                    if (!ok && lane == 0) *(volatile int*)&s_abort = 1;
+                    __syncwarp();
+                    nbar_arrive(kReady + (int)(g & 1), nthr);
+                    if (!ok) return;
+                    if (pending) publish();
+                    npub = 0;
+                    const bool last = q == RQ - 1;
+                    if (phase == 0) {
+                        if (!root) {
+                            pub_ptr[npub] = flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx);
+                            pub_val[npub++] = usent * 2 + (q + 1) * QS;
+                        }
+                        if (last)
+                            for (int k = 0; k < nchild; ++k) {
+                                pub_ptr[npub] = flag_ptr(P, child[k], F_TREE_UHEAD, c, 0);
+                                pub_val[npub++] = urecv[k] + 1;
+                            }
+                    } else {
+                        for (int k = 0; k < nchild; ++k) {
+                            pub_ptr[npub] = flag_ptr(P, child[k], F_TREE_DTAIL, c, 0);
+                            pub_val[npub++] = dsent * 2 + (q + 1) * QS;
+                        }
+                        if (last && !root) {
+                            pub_ptr[npub] = flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx);
+                            pub_val[npub++] = drecv + 1;
+                        }
+                    }
+                    pending = true;
+                    ++g;
+                }
+                if (phase == 0) {
+                    if (!root) ++usent;
+                    for (int k = 0; k < nchild; ++k) ++urecv[k];
+                } else {
+                    if (nchild) ++dsent;
+                    if (!root) ++drecv;
+                }
+            }
+        }
+        if (pending) publish();
+        if (lane == 0) {
+            st->tree_usent = usent;
+            st->tree_urecv[0] = urecv[0];
+            st->tree_urecv[1] = urecv[1];
+            st->tree_dsent = dsent;
+            st->tree_drecv = drecv;
+        }
+        return;
+    }
+    // -------------------------------------------------------------- data warps
+    const unsigned long long D = (unsigned long long)(nthr - 32), dt = (unsigned long long)(tid - 32);
+    unsigned long long g = 0;
+    for (int phase = 0; phase < 2; ++phase) {
+        for (unsigned long long sl = 0; sl < nslots; ++sl) {
+            const unsigned long long lo = ca + sl * SP, hi = (lo + SP < cb) ? lo + SP : cb;
+            for (int q = 0; q < RQ; ++q) {
+                const unsigned long long qs = lo + (hi - lo) * (unsigned long long)q / RQ;
+                const unsigned long long qe = lo + (hi - lo) * (unsigned long long)(q + 1) / RQ;
+                nbar_sync(kReady + (int)(g & 1), nthr);
+                if (*(volatile int*)&s_abort) return;
+                for (unsigned long long i0 = qs + dt; i0 < qe; i0 += U * D) {
+                    Batch<U> b;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        b.i[u] = i0 + u * D;
+                        b.j[u] = b.i[u] - lo;               // wire index in the slot
+                        b.in[u] = b.act[u] = b.i[u] < qe;
+                    }
+                    if (phase == 0) {
+                        uint4 own[U];
+                        load_batch<ES>(P, mine, b, own);
+                        uint4 in[2][U][AW];
+#pragma unroll
+                        for (int k = 0; k < 2; ++k)
+                            if (k < nchild) {
+                                const uint4* src = tree_up_slot<POLAR_PROTO_SIMPLE>(P, r, c, k, urecv[k]);
+#pragma unroll
+                                for (int u = 0; u < U; ++u)
+#pragma unroll
+                                    for (int x = 0; x < AW; ++x)
+                                        if (b.in[u]) in[k][u][x] = ld_cg(src + b.j[u] * AW + x);
+                            }
+                        uint4* dst = root ? nullptr : tree_up_slot<POLAR_PROTO_SIMPLE>(P, parent, c, my_child_idx, usent);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (!b.in[u]) continue;
+                            Acc<DT> acc;
+                            acc_init<DT>(acc, own[u]);
+#pragma unroll
+                            for (int k = 0; k < 2; ++k)
+                                if (k < nchild) {
+                                    Acc<DT> ch;
+#pragma unroll
+                                    for (int x = 0; x < AW; ++x) ch.w[x] = in[k][u][x];
+                                    acc_merge<DT, OP>(acc, ch);
+                                }
+                            if (root) store_pack<ES>(P, mine, b.i[u], acc_fin<DT>(acc));
+                            else
+#pragma unroll
+                                for (int x = 0; x < AW; ++x) W::put(P, dst, b.j[u] * AW + x, acc.w[x], 0);
+                        }
+                    } else {
+                        uint4 v[U];
+                        if (root) {
+                            load_batch<ES>(P, mine, b, v);
+                        } else {
+                            const uint4* src = tree_dn_slot<POLAR_PROTO_SIMPLE>(P, r, c, drecv);
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+                                if (b.in[u]) v[u] = ld_cg(src + b.j[u]);
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+                                if (b.in[u]) store_pack<ES>(P, mine, b.i[u], v[u]);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (b.in[u])
+                                for (int k = 0; k < nchild; ++k)
+                                    W::put(P, tree_dn_slot<POLAR_PROTO_SIMPLE>(P, child[k], c, dsent), b.j[u], v[u], 0);
+                    }
+                }
+                nbar_arrive(kDone + (int)(g & 1), nthr);
+                ++g;
+            }
+            if (phase == 0) {
+                if (!root) ++usent;
+                for (int k = 0; k < nchild; ++k) ++urecv[k];
+            } else {
+                if (nchild) ++dsent;
+                if (!root) ++drecv;
+            }
+        }
+    }
+}
+
+template <int DT, int OP>
+__device__ void tree_simple_ws(const Params& P, const Who& w) {
+    constexpr int ES = DType<DT>::ES;
+    constexpr int AW = AccWords<DT>::N;
+    unsigned long long ca, cb;
+    split_range(0, npacks<ES>(P), P.nch, w.c, ca, cb);
+    const unsigned long long SP = Wire<POLAR_PROTO_SIMPLE>::units(P.tree_slot) / AW;
+    // the same on every rank of a channel (ca, cb depend only on the channel)
+    if ((cb - ca + SP - 1) / SP <= 4 && (cb - ca) * 16ull >= 16384) tree_simple_ws_impl<DT, OP, 2>(P, w);
+    else tree_simple_ws_impl<DT, OP, 1>(P, w);
+}
+
 // ================================================================== kernels
 
 template <int DT, int OP, int ALGO, int PROTO>
@@ -1435,7 +1668,8 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
         if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_RING_WS) ring_simple_ws<DT, OP>(P, w);
         else ring<DT, OP, PROTO>(P, w);
     } else {
-        tree<DT, OP, PROTO>(P, w);
+        if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_TREE_WS) tree_simple_ws<DT, OP>(P, w);
+        else tree<DT, OP, PROTO>(P, w);
     }
     if (tel) {
         volatile TelEntry* e = P.tel + (P.seq % kTelRing);

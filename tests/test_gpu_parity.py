@@ -126,6 +126,30 @@ def test_back_to_back_alternating_no_sync():
         check_result([to_host(t, dtype) for t in ts], xs, dtype, "sum", algo, n)
 
 
+@pytest.mark.parametrize("algo", ["tree", "ring"])
+def test_simple_fifo_unit_sizes_back_to_back(algo):
+    """Warp-specialised ring/tree Simple (kernels.cuh ring_simple_ws /
+    tree_simple_ws): back-to-back calls whose channels hold 1 tiny slot, a few
+    slots (tree: half-slot units) and many slots (tree: whole-slot units) on one
+    stream without host sync, mixed with LL calls that advance the same FIFO
+    counters: the half-slot tail encoding must keep every wait exact."""
+    n, dtype = 8, "f32"
+    c = comm(n)
+    plan = [(1000, "simple", 4), ((1 << 20) // 4, "simple", 18), ((24 << 20) // 4, "simple", 18),
+            (777, "ll", 4), ((3 << 20) // 4 + 5, "simple", 8), (5, "simple", 2), ((40 << 20) // 4, "simple", 32),
+            ((1 << 20) // 4, "ll128", 18), ((2 << 20) // 4, "simple", 18)]
+    pending = []
+    for it, (count, proto, nch) in enumerate(plan * 2):
+        xs = synth.gen_ranks(dtype, count, n, cfg=300 + it, dist="ints")
+        ts = [to_device(x, dtype) for x in xs]
+        c.allreduce_forced(ts, algo, proto, nch)
+        pending.append((xs, ts))
+    torch.cuda.synchronize()
+    c.check()
+    for xs, ts in pending:
+        check_result([to_host(t, dtype) for t in ts], xs, dtype, "sum", algo, n)
+
+
 def test_policy_selected_decision_matches_oracle():
     """polar_allreduce (policy-selected): recorded decision == oracle mapping."""
     rows = [(0, 0, 16 << 10, OP.ONESHOT, OP.LL, 2), (0, 0, 256 << 10, OP.TWOSHOT, OP.LL, 4),
