@@ -1,5 +1,6 @@
 """Small parity subset for compute-sanitizer (memcheck / racecheck / synccheck):
-every algorithm x protocol, f32 + bf16, ragged counts, 3 virtual ranks, the TMA
+every algorithm x protocol, f32 + bf16, ragged counts (ring / tree Simple up to
+many FIFO slots per channel), 3 virtual ranks, the TMA
 two-shot, the direct collectives and the p2p probe; exits non-zero on a mismatch."""
 import os
 import sys
@@ -19,7 +20,9 @@ bad = 0
 for dtype in ("f32", "bf16"):
     for algo in ("oneshot", "twoshot", "ring", "tree"):
         for proto in ("ll", "ll128", "simple"):
-            for count in (7, 5003):
+            # ring / tree Simple also at multi-slot sizes (warp-specialised kernels:
+            # half-slot units, and the tree's whole-slot units beyond 4 slots per channel)
+            for count in ((7, 5003, 300_001, 1_300_001) if proto == "simple" and algo in ("ring", "tree") else (7, 5003)):
                 xs = synth.gen_ranks(dtype, count, n, cfg=5, dist="ints")
                 ts = [to_device(x, dtype) for x in xs]
                 c.allreduce_forced(ts, algo, proto, 2)
