@@ -8,6 +8,7 @@ Counts the instructions that evidence the design choices (B200_PROFILING.md
   UBLKCP.S.G / UBLKCP.G.S    TMA bulk copies global->smem / smem->global
   SYNCS.*                    mbarrier (transaction-count) operations
   MEMBAR.ALL.SYS / .GPU      release fences before flags
+  BAR.ARV / BAR.SYNC         named-barrier hand-offs (warp-specialised ring / tree Simple)
 """
 import argparse
 import collections
@@ -22,7 +23,7 @@ ALGO = {0: "tree", 1: "ring", 3: "oneshot", 4: "twoshot"}
 PROTO = {0: "ll", 1: "ll128", 2: "simple"}
 OP = {0: "sum", 2: "max", 3: "min"}
 PATS = ["LDG.E.128", "STG.E.128", "STRONG.SYS", "STRONG.GPU", "UBLKCP.S.G", "UBLKCP.G.S", "SYNCS", "SHFL", "VOTE",
-        "MEMBAR.ALL.SYS", "MEMBAR.ALL.GPU", "FADD", "NANOSLEEP"]
+        "MEMBAR.ALL.SYS", "MEMBAR.ALL.GPU", "FADD", "NANOSLEEP", "BAR.ARV", "BAR.SYNC"]
 
 
 def main():
