@@ -165,6 +165,35 @@ def main():
     comm.check()
     for (xs, algo), t in zip(xss, ts):
         check(f"b2b/{algo}", t, xs, "i32", "sum", True)
+    # CUDA-graph capture on the real (IPC) comm: registered zero-copy two-shot,
+    # warp-specialised ring and tree Simple (multi-slot), ring LL; every replay
+    # advances the device-resident epochs / FIFO counters, none is host-synced
+    # between the captured calls
+    plan = [("twoshot", "simple", 50_003), ("ring", "simple", 400_001), ("tree", "simple", 1_000_003),
+            ("ring", "ll", 20_011)]
+    (gsym,) = comm.mem_alloc_tensors(plan[0][2], torch.float32)
+    gbufs = [gsym] + [torch.empty(c, dtype=torch.float32, device="cuda") for _, _, c in plan[1:]]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for (algo, proto, _), b in zip(plan, gbufs):
+            comm.allreduce_forced(b, algo, proto, 4)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for (algo, proto, _), b in zip(plan, gbufs):
+            comm.allreduce_forced(b, algo, proto, 4)
+    for rep in range(3):
+        xss = [synth.gen_ranks("f32", c, ws, cfg=60 + 10 * rep + i, dist="ints") for i, (_, _, c) in enumerate(plan)]
+        for xs, b in zip(xss, gbufs):
+            b.copy_(torch.from_numpy(xs[rank]))
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        comm.check()
+        for (algo, proto, _), xs, b in zip(plan, xss, gbufs):
+            check(f"graph{rep}/{algo}/{proto}", b, xs, "f32", "sum", True)
+    del g, gbufs, gsym
     comm.destroy()
     allres = [None] * ws
     dist.all_gather_object(allres, results)
