@@ -1070,6 +1070,27 @@ __device__ void ring(const Params& P, const Who& w) {
 #ifndef POLAR_RING_WS_BATCH
 #define POLAR_RING_WS_BATCH POLAR_BATCH_SIMPLE   // packs per data thread per iteration (f32)
 #endif
+#ifndef POLAR_WS_PREFETCH
+#define POLAR_WS_PREFETCH 0
+#endif
+// The sync warp warms L2 with the data warps' NEXT own-buffer range (ring
+// reduce-scatter steps, tree up slots): one cp.async.bulk.prefetch.L2 per 32 KiB,
+// no registers, so the data warps' own loads hit L2 instead of HBM.  Only full,
+// 16-B aligned packs (P.vec; the partial last pack is never prefetched).
+// Off by default: measured no gain (profiles/r01_ws_prefetch_ab.jsonl: ring
+// 128 MiB 927 -> 932 us, 1 MiB 39.9 -> 43.3 us; tree 128 MiB 1100 -> 1083 us) —
+// the data warps are not waiting on their own-buffer loads.
+__device__ __forceinline__ void prefetch_own(const Params& P, const char* base, unsigned long long a,
+                                             unsigned long long b, unsigned long long full) {
+#if POLAR_WS_PREFETCH
+    if (!P.vec) return;
+    if (b > full) b = full;
+    for (unsigned long long o = a; o < b; o += 2048) {
+        const unsigned long long e = (b - o < 2048) ? b - o : 2048;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o * 16), "r"((unsigned)(e * 16)) : "memory");
+    }
+#endif
+}
 __device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 
@@ -1096,6 +1117,7 @@ __device__ void ring_simple_ws(const Params& P, const Who& w) {
     split_range(0, NP, P.nch, c, ca, cb);
     char* mine = P.bufs[r];
     const unsigned long long LC = SP * (unsigned long long)n;
+    const unsigned long long full_packs = P.count * (unsigned long long)ES / 16;   // whole 16-B packs
     __shared__ int s_abort;
     if (tid == 0) s_abort = 0;
     __syncthreads();
@@ -1132,6 +1154,19 @@ __device__ void ring_simple_ws(const Params& P, const Who& w) {
                     nbar_arrive(kReady + (int)(g & 1), nthr);
                     if (!ok) return;
                     if (g > 0) publish();
+                    if (POLAR_WS_PREFETCH && lane == 0 && q == 0) {
+                        // own slice of the next reduce-scatter step (or the next lap's step 0)
+                        const bool nxt_lap = s == 2 * (n - 1);
+                        if (s + 1 < n || nxt_lap) {
+                            const unsigned long long b2 = nxt_lap ? base + LC : base;
+                            if (b2 < cb) {
+                                const unsigned long long L2 = (cb - b2 < LC) ? cb - b2 : LC;
+                                const int k2 = nxt_lap ? r : ((r - (s + 1)) % n + n) % n;
+                                prefetch_own(P, mine, b2 + L2 * (unsigned long long)k2 / n,
+                                             b2 + L2 * (unsigned long long)(k2 + 1) / n, full_packs);
+                            }
+                        }
+                    }
                     pub_tail = do_send ? sent * RQ + q + 1 : 0;
                     pub_head = (do_recv && q == RQ - 1) ? recvd + 1 : 0;
                     ++g;
@@ -1502,6 +1537,10 @@ __device__ void tree_simple_ws_impl(const Params& P, const Who& w) {
                     nbar_arrive(kReady + (int)(g & 1), nthr);
                     if (!ok) return;
                     if (pending) publish();
+                    if (POLAR_WS_PREFETCH && phase == 0 && q == 0 && lane == 0 && sl + 1 < nslots) {
+                        const unsigned long long a2 = ca + (sl + 1) * SP;   // own range of the next up slot
+                        prefetch_own(P, mine, a2, (a2 + SP < cb) ? a2 + SP : cb, P.count * (unsigned long long)ES / 16);
+                    }
                     npub = 0;
                     const bool last = q == RQ - 1;
                     if (phase == 0) {
