@@ -1091,6 +1091,20 @@ __device__ __forceinline__ void prefetch_own(const Params& P, const char* base, 
     }
 #endif
 }
+// wait_geq with a per-lane cache of the last value acquired from *p (monotone
+// flags): skips the load when an earlier acquire already covers v (that acquire
+// still orders everything after it)
+#ifndef POLAR_WS_CACHED_POLL
+#define POLAR_WS_CACHED_POLL 1
+#endif
+__device__ __forceinline__ bool wait_cached(const Params& P, const uint64_t* p, uint64_t v, uint64_t& seen) {
+    if (POLAR_WS_CACHED_POLL && seen >= v) return true;
+    seen = ld_acquire(p, P.sys);
+    if (seen >= v) return true;
+    if (!wait_geq_slow(p, v, P.sys, P.timeout_ns, P.err)) return false;
+    seen = v;
+    return true;
+}
 __device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 
@@ -1130,6 +1144,7 @@ __device__ void ring_simple_ws(const Params& P, const Who& w) {
         uint64_t* tail_out = flag_ptr(P, next, F_RING_TAIL, c, 0);
         uint64_t* head_out = flag_ptr(P, prev, F_RING_HEAD, c, 0);
         unsigned long long g = 0;
+        uint64_t seen = 0;                                // lane 0: last fill, lane 1: last credit acquired
         uint64_t pub_tail = 0, pub_head = 0;              // unit g-1's flag values (0: none)
         auto publish = [&]() {
             nbar_sync(kDone + (int)((g - 1) & 1), nthr);  // unit g-1 moved by every data warp
@@ -1143,14 +1158,16 @@ __device__ void ring_simple_ws(const Params& P, const Who& w) {
             for (int s = 0; s < 2 * (n - 1) + 1; ++s) {
                 const bool do_recv = s > 0, do_send = s < 2 * (n - 1);
                 for (int q = 0; q < RQ; ++q) {
+                    // lane 0: the fill, lane 1: the credit, in parallel; each lane
+                    // keeps the last value it acquired (flags are monotone), so a
+                    // unit already covered by an earlier load costs no round trip
                     int ok = 1;
-                    if (lane == 0) {
-                        if (do_recv) ok = wait_geq(P, tail_in, recvd * RQ + q + 1);
-                        if (ok && q == 0 && do_send && sent >= (unsigned long long)kSteps)
-                            ok = wait_geq(P, head_in, sent - kSteps + 1);
-                        if (!ok) *(volatile int*)&s_abort = 1;
-                    }
-                    ok = __shfl_sync(0xffffffffu, ok, 0);
+                    if (lane == 0 && do_recv) ok = wait_cached(P, tail_in, recvd * RQ + q + 1, seen);
+                    if (lane == 1 && q == 0 && do_send && sent >= (unsigned long long)kSteps)
+                        ok = wait_cached(P, head_in, sent - kSteps + 1, seen);
+                    ok = __all_sync(0xffffffffu, ok);
+                    if (!ok && lane == 0) *(volatile int*)&s_abort = 1;
+                    __syncwarp();
                     nbar_arrive(kReady + (int)(g & 1), nthr);
                     if (!ok) return;
                     if (g > 0) publish();
