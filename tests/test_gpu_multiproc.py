@@ -28,12 +28,16 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("nranks,tma", [(2, "0"), (3, "0"), (2, "1")])
-def test_multiprocess_ipc_all_algorithms(tmp_path, nranks, tma):
-    """tma=1: the TMA-staged two-shot (cp.async.bulk) on CUDA-IPC-mapped peer memory."""
+@pytest.mark.parametrize("nranks,tma,jitter", [(2, "0", "0"), (3, "0", "0"), (2, "1", "0"), (3, "0", "20000")])
+def test_multiprocess_ipc_all_algorithms(tmp_path, nranks, tma, jitter):
+    """tma=1: the TMA-staged two-shot (cp.async.bulk) on CUDA-IPC-mapped peer memory.
+    jitter: random __nanosleep (< 20 us) before 1/8 of all signal / LL stores in
+    every process (sys-scope flags, the warp-specialised ring/tree publishers
+    included): every result must stay exact under skewed arrival orders."""
     out = tmp_path / "mp.json"
     env = dict(os.environ)
     env["POLAR_TWOSHOT_TMA"] = tma
+    env["POLAR_JITTER_NS"] = jitter
     env.setdefault("POLAR_TIMEOUT_MS", "60000")
     env["POLAR_BOUNCE"] = str(1 << 20)   # small bounce buffer: exercise the chunked bounce path
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
