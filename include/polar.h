@@ -20,6 +20,12 @@
  *     time.  Policy functions are process-global and thread-safe.
  *   - Errors raised on the device (a peer that never arrives) are latched in the
  *     comm and returned by the NEXT call on it, or by polar_comm_check().
+ *   - Cross-rank consistency (the paper is silent, DESIGN.md
+ *     R12): on a real comm every launch carries a decision tag (kind, algorithm,
+ *     protocol, channels, dtype, op, count, root).  Each rank publishes its tag
+ *     in its scratch and compares its peers' tags of the PREVIOUS launch; a
+ *     difference (a policy swapped on one rank only, mismatched counts or ops)
+ *     latches POLAR_ESTATE, one launch late, instead of going unnoticed.
  */
 #ifndef POLAR_H
 #define POLAR_H
@@ -304,8 +310,10 @@ polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint
 /* Number of kernels this comm has launched so far (evidence for bench.py). */
 uint64_t polar_comm_launches(polar_comm_t comm);
 
-/* Latched asynchronous errors (device timeouts); POLAR_OK if none.  Does not
- * synchronise: a timeout becomes visible once the kernel that hit it ended. */
+/* Latched asynchronous errors (device timeouts: POLAR_ETIMEOUT; ranks whose
+ * launches disagreed: POLAR_ESTATE); POLAR_OK if none.  Does not synchronise: an
+ * error becomes visible once the kernel that raised it ended (a disagreement at
+ * launch k is raised by launch k + 1). */
 polar_status polar_comm_check(polar_comm_t comm);
 
 /* Diagnostics: when dev_buf is non-NULL, every CTA of every later AllReduce on

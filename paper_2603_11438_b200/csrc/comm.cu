@@ -54,6 +54,7 @@ Layout make_layout(bool with_bounce) {
     size_t off = 0;
     L.flags_off = off; off = align_up(off + kFlagBytes, 4096);
     L.state_off = off; off = align_up(off + kStateBytes, 4096);
+    L.tags_off = off; off = align_up(off + kTagRing * 16, 4096);
     L.os_chunk = align_up(env_size("POLAR_OS_CHUNK", 1 << 20), 512);
     L.os_off = off; off = align_up(off + 2 * kMaxRanks * L.os_chunk, 4096);
     L.osll_chunk = align_up(env_size("POLAR_OSLL_CHUNK", 256 << 10), 512);
@@ -107,6 +108,8 @@ struct polar_comm_s {
     polar_decision last{};
     uint32_t last_nch = 0;
     uint64_t launches = 0;
+    uint64_t calls = 0;                  // collective launches on this comm (identical on every rank)
+    uint64_t prev_tag = 0;               // decision tag of the previous launch
     polar_status latched = POLAR_OK;
     polar_allgather_fn ag = nullptr;
     void* user = nullptr;
@@ -175,7 +178,7 @@ void fill_params(const polar_comm_s* c, dev::Params& P) {
     P.err = c->err_dev;
     P.timeout_ns = c->timeout_ns;
     const Layout& L = c->L;
-    P.flags_off = L.flags_off; P.state_off = L.state_off;
+    P.flags_off = L.flags_off; P.state_off = L.state_off; P.tags_off = L.tags_off;
     P.os_off = L.os_off; P.os_chunk = L.os_chunk;
     P.osll_off = L.osll_off; P.osll_chunk = L.osll_chunk;
     P.tsll_off = L.tsll_off; P.tsll_chunk = L.tsll_chunk;
@@ -198,8 +201,22 @@ polar_status check_latched(polar_comm_s* c) {
     return c->latched;
 }
 
+// Decision tag of one launch (SURVEY.md §8(b) "cross-rank consistency"): every
+// field that must agree across ranks for the exchange to be correct.
+uint64_t decision_tag(int kind, int algo, int proto, int nch, int dtype, int op, uint64_t count, int root) {
+    uint64_t h = ((uint64_t)kind) | ((uint64_t)algo << 4) | ((uint64_t)proto << 8) | ((uint64_t)nch << 12) |
+                 ((uint64_t)dtype << 20) | ((uint64_t)op << 26) | ((uint64_t)(root & 0xff) << 30);
+    h ^= count * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 29;
+    return h | 1;   // never 0
+}
+
 polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int grid, cudaStream_t stream,
                           size_t smem = 0) {
+    // real comms: the kernel publishes P.dtag for launch P.call and checks the
+    // peers' tags of the previous launch against P.prev_tag (kernels.cuh tag_begin/end)
+    P.call = c->calls;
+    P.prev_tag = c->prev_tag;
     void* args[] = {&P};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -233,6 +250,8 @@ polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int 
         return POLAR_ECUDA;
     }
     c->launches++;
+    c->calls++;
+    c->prev_tag = P.dtag;
     return POLAR_OK;
 }
 
@@ -492,6 +511,9 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     fill_params(c, P);
     P.nch = (int)d.nchannels;
     const int grid = c->nlocal * P.nch;
+    // the bounce path launches per chunk: each launch's count is in its own tag
+    auto tag_for = [&](size_t cnt) { return decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, cnt, 0); };
+    P.dtag = tag_for(count);
     if (c->ad.prm.enabled) {
         adaptive_drain(c);           // keep the ring from lapping between windows
         P.tel = c->tel_dev;
@@ -543,6 +565,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         char* src = mine + done * es;
         CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, stream));
         P.count = n;
+        P.dtag = tag_for(n);
         st = launch_kernel(c, fn, P, grid, stream, smem);
         if (st != POLAR_OK) return st;
         CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, stream));
@@ -594,6 +617,7 @@ polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* cons
     P.nch = (int)d.nchannels;
     P.count = count;
     P.root = root;
+    P.dtag = decision_tag(1 + mode, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, root);
     const int grid = c->nlocal * P.nch;
     bool vec = mode == 2 || (blk % 16) == 0;
     auto aligned = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };

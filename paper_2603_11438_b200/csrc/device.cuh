@@ -47,6 +47,11 @@ struct Params {
                                 // signal and LL stores (POLAR_JITTER_NS; 0 = off)
     TelEntry* tel;              // profiler telemetry ring (host-mapped), or null
     unsigned long long seq;     // this launch's sequence number in the ring
+    // cross-rank decision check (real comms; kernels.cuh tag_begin / tag_end)
+    unsigned long long tags_off;  // tag ring in every rank's scratch
+    unsigned long long call;      // this launch's index on the comm (same on every rank)
+    unsigned long long dtag;      // this launch's decision tag
+    unsigned long long prev_tag;  // the previous launch's tag (call - 1)
     // direct collectives (ReduceScatter / AllGather / Broadcast)
     char* recv[kMaxRanks];      // rank p's receive buffer (RS / AG), peer-mapped
     int root;                   // Broadcast root

@@ -1700,6 +1700,48 @@ __device__ void tree_simple_ws(const Params& P, const Who& w) {
     else tree_simple_ws_impl<DT, OP, 1>(P, w);
 }
 
+// ============================================== cross-rank decision check
+// SURVEY.md §8(b) "cross-rank consistency" (R12): on a real comm every
+// rank decides locally, so ranks that disagree (a policy swapped on one rank
+// only, different counts, ops or channel counts) would exchange mismatched data
+// — silently wrong results or a timeout.  Each launch's thread 0 of CTA 0
+//   tag_begin: publishes {call, tag} in its own scratch ring and issues
+//              cp.async copies of every peer's entry for call - 1 into shared
+//              memory (no registers held, the NVLink round trip overlaps the
+//              collective);
+//   tag_end:   waits for the copies and latches POLAR_ESTATE if a peer's entry
+//              for call - 1 carries a different tag.
+// Detection is one launch late and never a false positive: an entry whose call
+// stamp is not call - 1 (not yet visible) is skipped.  Each 8-B half of the
+// 16-B entry carries the call stamp ({tag_lo, call}, {tag_hi, call}), so a torn
+// read is rejected, not misread.  Virtual comms decide once for all ranks.
+__device__ __forceinline__ const char* tag_entry(const Params& P, int rank, unsigned long long call) {
+    return P.scratch[rank] + P.tags_off + (call % kTagRing) * 16;
+}
+__device__ __forceinline__ void tag_begin(const Params& P, uint4* s_tags) {
+    if (!P.sys || blockIdx.x != 0 || threadIdx.x != 0) return;
+    const uint32_t c = (uint32_t)P.call;
+    st_ll(reinterpret_cast<uint4*>(const_cast<char*>(tag_entry(P, P.rank0, P.call))), (uint32_t)P.dtag,
+          (uint32_t)(P.dtag >> 32), c);
+    if (P.call == 0) return;
+    for (int p = 0; p < P.nranks; ++p)
+        if (p != P.rank0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&s_tags[p])),
+                         "l"(tag_entry(P, p, P.call - 1))
+                         : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tag_end(const Params& P, const uint4* s_tags) {
+    if (!P.sys || blockIdx.x != 0 || threadIdx.x != 0 || P.call == 0) return;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const uint32_t c = (uint32_t)(P.call - 1);
+    for (int p = 0; p < P.nranks; ++p) {
+        if (p == P.rank0) continue;
+        const uint4 t = s_tags[p];
+        if (t.y == c && t.w == c && (t.x | ((unsigned long long)t.z << 32)) != P.prev_tag) raise_error(P, POLAR_ESTATE);
+    }
+}
+
 // ================================================================== kernels
 
 template <int DT, int OP, int ALGO, int PROTO>
@@ -1710,6 +1752,8 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
     // when the launch carries no PDL attribute).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ __align__(16) uint4 s_tags[kMaxRanks];
+    tag_begin(P, s_tags);
     const Who w = who(P);
     // profiler telemetry (f3): CTA 0 stamps the launch into the host-mapped ring
     const bool tel = P.tel != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
@@ -1727,6 +1771,7 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
         if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_TREE_WS) tree_simple_ws<DT, OP>(P, w);
         else tree<DT, OP, PROTO>(P, w);
     }
+    tag_end(P, s_tags);
     if (tel) {
         volatile TelEntry* e = P.tel + (P.seq % kTelRing);
         e->t0 = tel_t0;
@@ -1753,6 +1798,8 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr int ES = DType<DT>::ES;
+    __shared__ __align__(16) uint4 s_tags[kMaxRanks];
+    tag_begin(P, s_tags);
     const Who w = who(P);
     const int n = w.n, tid = w.tid;
     ChanState* st = chan_state(P, w.r, w.c);
@@ -1811,6 +1858,7 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) direct_kernel(Params P) 
     __syncthreads();
     if (!handshake_exit(P, w, e)) return;
     epoch_publish(P, w, e);
+    tag_end(P, s_tags);
 }
 
 }  // namespace dev

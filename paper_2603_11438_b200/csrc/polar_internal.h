@@ -51,9 +51,11 @@ struct ChanState {
     uint64_t pad[7];
 };
 constexpr size_t kStateBytes = sizeof(ChanState) * kMaxCh;
+constexpr unsigned long long kTagRing = 64;   // launches remembered per rank for the decision check
 
 struct Layout {
     size_t flags_off, state_off;
+    size_t tags_off;                  // decision tags: [kTagRing] x 16 B (real comms, cross-rank check)
     size_t os_off, os_chunk;          // one-shot Simple staging: [2][kMaxRanks][os_chunk]
     size_t osll_off, osll_chunk;      // one-shot LL: [2][kMaxRanks][2*osll_chunk] (payload bytes per slot)
     size_t tsll_off, tsll_chunk;      // two-shot LL: RS [2][R][2*c] then AG [2][R][2*c]

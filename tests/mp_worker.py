@@ -194,6 +194,24 @@ def main():
         for (algo, proto, _), xs, b in zip(plan, xss, gbufs):
             check(f"graph{rep}/{algo}/{proto}", b, xs, "f32", "sum", True)
     del g, gbufs, gsym
+    # cross-rank decision check (kernels.cuh tag_begin/tag_end):
+    # every call above was consistent, so nothing may have latched; then rank 0
+    # alone asks for MAX where the others ask for SUM (same algorithm, count and
+    # channels, so the exchange completes with silently mixed results) — the next
+    # launch must latch POLAR_ESTATE on every rank
+    comm.check()
+    xs = synth.gen_ranks("f32", 10_001, ws, cfg=90, dist="ints")
+    t = to_device(xs[rank], "f32")
+    comm.allreduce_forced(t, "twoshot", "ll", 2, op="max" if rank == 0 else "sum")
+    comm.allreduce_forced(t, "twoshot", "ll", 2)
+    torch.cuda.synchronize()
+    try:
+        comm.check()
+        latched = None
+    except L.PolarError as ex:
+        latched = ex.name
+    results.append({"tag": "decision-mismatch-latched", "rank": rank, "ok": latched == "estate", "identical": True,
+                    "latched": latched})
     comm.destroy()
     allres = [None] * ws
     dist.all_gather_object(allres, results)
