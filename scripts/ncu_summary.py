@@ -27,7 +27,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
         "sm__maximum_warps_per_active_cycle_pct", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
         "smsp__average_warp_latency_issue_stalled_long_scoreboard", "smsp__cycles_active.avg",
-        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum"]
+        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"]
 
 
 def launch_shares(tag):
@@ -74,6 +76,10 @@ def full_metrics(tag, workload):
                 i = hdr.index(k)
                 lines.append(f"  {k} = {v[i]} {units[i]}")
                 d[k] = (v[i], units[i])
+        for op in ("ld", "st"):   # 16 sectors per request = full-warp 16-B accesses
+            ks, kr = f"l1tex__t_sectors_pipe_lsu_mem_global_op_{op}.sum", f"l1tex__t_requests_pipe_lsu_mem_global_op_{op}.sum"
+            if ks in d and kr in d and float(d[kr][0]) > 0:
+                lines.append(f"  global {op} sectors/request = {float(d[ks][0]) / float(d[kr][0]):.2f}")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         if "dram__bytes_read.sum" in d:
             rb = float(d["dram__bytes_read.sum"][0]) * scale[d["dram__bytes_read.sum"][1]]
