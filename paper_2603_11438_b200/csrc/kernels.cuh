@@ -1338,9 +1338,11 @@ __device__ void tree(const Params& P, const Who& w) {
     for (unsigned long long s = 0; s < nslots; ++s) {
         const unsigned long long lo = ca + s * SP, hi = (lo + SP < cb) ? lo + SP : cb;
         bool ok = true;
-        // thread k waits for child k's fill, thread 2 for the parent's credit
+        // thread k waits for child k's fill, thread 2 for the parent's credit.
+        // Simple tails count HALF slots (2 per slot), the unit of tree_simple_ws,
+        // which runs the same FIFOs for larger calls
         if (PROTO == POLAR_PROTO_SIMPLE && tid < nchild)
-            ok = wait_geq(P, flag_ptr(P, r, F_TREE_UTAIL, c, tid), urecv[tid] + 1);
+            ok = wait_geq(P, flag_ptr(P, r, F_TREE_UTAIL, c, tid), 2 * (urecv[tid] + 1));
         if (tid == 2 && !root && usent >= (unsigned long long)kSteps)
             ok = wait_geq(P, flag_ptr(P, r, F_TREE_UHEAD, c, 0), usent - kSteps + 1);
         if (!__syncthreads_and(ok)) return;
@@ -1407,7 +1409,7 @@ __device__ void tree(const Params& P, const Who& w) {
         if (tid == 0) {
             if (PROTO == POLAR_PROTO_SIMPLE && (!root || (POLAR_DISCARD && nchild))) fence_acq_rel(P.sys);
             if (!root && PROTO == POLAR_PROTO_SIMPLE)
-                jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), usent + 1, P.sys);
+                jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_UTAIL, c, my_child_idx), 2 * (usent + 1), P.sys);
             for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_UHEAD, c, 0), urecv[k] + 1, P.sys);
         }
         if (!root) ++usent;
@@ -1418,7 +1420,7 @@ __device__ void tree(const Params& P, const Who& w) {
         const unsigned long long lo = ca + s * SP, hi = (lo + SP < cb) ? lo + SP : cb;
         bool ok = true;
         // thread 0: the parent's fill; threads 1, 2: the children's credits
-        if (tid == 0 && !root && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), drecv + 1);
+        if (tid == 0 && !root && PROTO == POLAR_PROTO_SIMPLE) ok = wait_geq(P, flag_ptr(P, r, F_TREE_DTAIL, c, 0), 2 * (drecv + 1));
         if (tid >= 1 && tid <= nchild && dsent >= (unsigned long long)kSteps)
             ok = wait_geq(P, flag_ptr(P, r, F_TREE_DHEAD, c, tid - 1), dsent - kSteps + 1);
         if (!__syncthreads_and(ok)) return;
@@ -1451,7 +1453,7 @@ __device__ void tree(const Params& P, const Who& w) {
         if (tid == 0) {
             if (PROTO == POLAR_PROTO_SIMPLE && (nchild || (POLAR_DISCARD && !root))) fence_acq_rel(P.sys);
             if (PROTO == POLAR_PROTO_SIMPLE && nchild)
-                for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), dsent + 1, P.sys);
+                for (int k = 0; k < nchild; ++k) jitter(P), st_relaxed(flag_ptr(P, child[k], F_TREE_DTAIL, c, 0), 2 * (dsent + 1), P.sys);
             if (!root) jitter(P), st_relaxed(flag_ptr(P, parent, F_TREE_DHEAD, c, my_child_idx), drecv + 1, P.sys);
         }
         if (nchild) ++dsent;
@@ -1688,6 +1690,9 @@ __device__ void tree_simple_ws_impl(const Params& P, const Who& w) {
     }
 }
 
+#ifndef POLAR_TREE_WS_MIN
+#define POLAR_TREE_WS_MIN 16384   // bytes per channel below which tree Simple runs the plain kernel
+#endif
 template <int DT, int OP>
 __device__ void tree_simple_ws(const Params& P, const Who& w) {
     constexpr int ES = DType<DT>::ES;
@@ -1695,8 +1700,12 @@ __device__ void tree_simple_ws(const Params& P, const Who& w) {
     unsigned long long ca, cb;
     split_range(0, npacks<ES>(P), P.nch, w.c, ca, cb);
     const unsigned long long SP = Wire<POLAR_PROTO_SIMPLE>::units(P.tree_slot) / AW;
-    // the same on every rank of a channel (ca, cb depend only on the channel)
-    if ((cb - ca + SP - 1) / SP <= 4 && (cb - ca) * 16ull >= 16384) tree_simple_ws_impl<DT, OP, 2>(P, w);
+    // the same on every rank of a channel (ca, cb depend only on the channel).
+    // Below 16 KiB per channel the plain tree (one slot, no hand-offs) is faster
+    // (4-64 KiB: 17.7 vs 19.7-20.1 us); its Simple tails count half slots too
+    const unsigned long long bytes = (cb - ca) * 16ull;
+    if (bytes < POLAR_TREE_WS_MIN) tree<DT, OP, POLAR_PROTO_SIMPLE>(P, w);
+    else if ((cb - ca + SP - 1) / SP <= 4) tree_simple_ws_impl<DT, OP, 2>(P, w);
     else tree_simple_ws_impl<DT, OP, 1>(P, w);
 }
 
