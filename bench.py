@@ -7,22 +7,29 @@ N = 1 (no torchrun): 8 VIRTUAL ranks on cuda:0,
     made by the policy hook each call.  All ranks' traffic shares one HBM, so the
     roofline is HBM: every step must read n x S and write n x S bytes.
 N > 1 (torchrun, one rank per GPU): real ranks over NVLink/NVSwitch with CUDA
-    IPC peer mappings, same message; NCCL's default AllReduce is timed beside
-    it on the same buffers for the "speedup vs NCCL default" half of the metric.
+    IPC peer mappings, same message; NCCL's default AllReduce (ctypes
+    libnccl.so.2, no NCCL_* overrides, its choice read from its TUNING log) is
+    timed on the SAME buffers and stream for the "speedup vs NCCL default" half
+    of the metric, over the whole 4 KiB - 1 GiB sweep (BASELINE configs 2-3).
 
 A step = one policy-selected polar AllReduce (decide + one kernel launch) of the
 workload.  Timing: W warm-up steps, then K steps between CUDA events on the
 launching stream, barrier + synchronize on both sides, max over ranks.  The
 n x 128 MiB inputs exceed the 126 MB L2, so no flush is needed between steps.
+After the timed region the same buffers are re-filled, one step of the same
+launch configuration runs again and sampled windows are checked against the
+oracle (`parity`; a busBW is never printed for wrong data without saying so).
 --impl reference times the CPU oracle (oracle/) on the host cores instead.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
 import sys
+import tempfile
 import threading
 import time
 
@@ -33,7 +40,11 @@ METRIC = "AllReduce busBW GB/s vs size at 2/4/8 B200; speedup vs NCCL default"
 S_BYTES = 128 << 20            # BASELINE config 2 headline size (per rank)
 VIRTUAL_RANKS = 8
 C2_SIZES = [4 << 20, 8 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20]
+NVLINK_SIZES = [(4 << 10) << k for k in range(19)]    # 4 KiB .. 1 GiB (BASELINE config 3)
+L2_BYTES = 126 << 20
+NVLINK_GBS = 900.0             # per direction per GPU (PAPER.md L414 / BJ; R11)
 PAPER_8GPU_128MIB_DEFAULT = 596.9   # PAPER.md Table 2 L559 (8x B300, NCCL NVLS) — context
+U64_MAX = 2**64 - 1
 
 
 def busbw(nbytes, n, t):
@@ -55,6 +66,17 @@ def load_traffic():
         with open(p) as f:
             return json.load(f)
     return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -113,19 +135,30 @@ def env_dist():
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-# ------------------------------------------------------------------ reference
+# ------------------------------------------------------------------ CPU oracle legs
+def _oracle_workload(n, count):
+    import synth
+    return synth.gen_ranks("f32", count, n, cfg=2, dist="unif")
+
+
+def _sample_text(n, count, cores, extra=""):
+    return (f"{n} ranks x {count} f32 ({count * 4 / 2**20:.1f} MiB/rank) of the {S_BYTES >> 20} MiB/rank C2 workload, "
+            f"plain C oracle (oracle/c/allreduce_ref.c) on {cores} threads of '{cpu_model()}'{extra}")
+
+
 def run_reference(args):
-    """The CPU oracle, as it stands, timed on the host cores (rank 0 only)."""
+    """The CPU oracle, as it stands, timed on the host cores (rank 0 only).
+    Each step is the FULL C2 workload (n x 128 MiB) when K + W steps fit the
+    ~2-minute budget, else the same leading fraction of every rank's input."""
     ws, rank, _ = env_dist()
     if rank != 0:
         return
-    import synth
     from oracle import cref
 
     n = VIRTUAL_RANKS if ws == 1 else ws
     cores = len(os.sched_getaffinity(0))
     count_full = S_BYTES // 4
-    xs_full = synth.gen_ranks("f32", count_full, n, cfg=2, dist="unif")
+    xs_full = _oracle_workload(n, count_full)
 
     def oracle(xs):
         return cref.allreduce(xs, "f32", "sum", cores)
@@ -146,14 +179,14 @@ def run_reference(args):
         ts.append(time.perf_counter() - t0)
     t = sum(ts) / len(ts)
     v = busbw(count * 4, n, t)
-    sample = (f"{n} ranks x {count} f32 ({count * 4 / 2**20:.1f} MiB/rank) of the {S_BYTES >> 20} MiB workload, "
-              f"plain C oracle (oracle/c/allreduce_ref.c) on {cores} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(n, ws > 1),
-        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": _sample_text(n, count, cores, f", mean of {args.steps} steps"),
+                         "cpu_model": cpu_model()},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -163,11 +196,11 @@ def workload_config(n, real):
         "workload": (f"C2 {n}-rank AllReduce fp32 sum, {S_BYTES >> 20} MiB per rank, policy-selected, "
                      + ("real ranks (1 per GPU, NVLink)" if real else f"{n} virtual ranks on 1 B200")),
         "nranks": n, "bytes_per_rank": S_BYTES, "op": "sum", "dtype": "f32",
+        "buffers": "symmetric (polar_mem_alloc: registered, zero-copy two-shot)",
         "l2": f"inputs larger than L2 ({n} x {S_BYTES >> 20} MiB resident), no flush",
     }
 
 
-# ------------------------------------------------------------------ cpu baseline leg
 def _time_oracle(fn, budget_s, max_runs=200):
     ts = []
     t_end = time.perf_counter() + budget_s
@@ -180,22 +213,23 @@ def _time_oracle(fn, budget_s, max_runs=200):
     return statistics.median(ts), len(ts)
 
 
-def cpu_baseline(n, count):
-    """The oracle timed on the host: the plain threaded C oracle on every core
-    this process may run on, and the numpy oracle on 1 core."""
-    import synth
+def cpu_baseline(n, count, xs=None):
+    """The oracle timed on the host on the SAME workload the reference arm times
+    (the full n x 128 MiB C2 message): the plain threaded C oracle on every core
+    this process may run on, and the numpy oracle on 1 core on
+    a 1/16 sample of it (it needs ~0.5 s per MiB of ranks' input)."""
     from oracle import allreduce as orc
     from oracle import cref
-    sub = min(count, 8 << 20)
-    xs = synth.gen_ranks("f32", sub, n, cfg=2, dist="unif")
+    xs = xs if xs is not None else _oracle_workload(n, count)
     cores = len(os.sched_getaffinity(0))
-    t_c, runs_c = _time_oracle(lambda: cref.allreduce(xs, "f32", "sum", cores), 10.0)
-    t_np, runs_np = _time_oracle(lambda: orc.allreduce(xs, "f32", "sum"), 5.0)
-    return {"value": round(busbw(sub * 4, n, t_c), 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} ranks x {sub} f32 ({sub * 4 >> 20} MiB/rank) of the C2 workload, plain C oracle "
-                      f"(oracle/c/allreduce_ref.c) on {cores} threads, median of {runs_c} runs",
+    t_c, runs_c = _time_oracle(lambda: cref.allreduce(xs, "f32", "sum", cores), 10.0, max_runs=20)
+    sub = count // 16
+    xsub = [x[:sub] for x in xs]
+    t_np, runs_np = _time_oracle(lambda: orc.allreduce(xsub, "f32", "sum"), 5.0)
+    return {"value": round(busbw(count * 4, n, t_c), 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": _sample_text(n, count, cores, f", median of {runs_c} runs"), "cpu_model": cpu_model(),
             "numpy_1core": {"value": round(busbw(sub * 4, n, t_np), 3), "unit": "GB/s", "cores": 1,
-                            "runs": runs_np}}
+                            "runs": runs_np, "sample": f"{n} ranks x {sub} f32 (1/16 of the workload)"}}
 
 
 def decision_cost(L):
@@ -205,9 +239,65 @@ def decision_cost(L):
             "timer_overhead_ns": s["timer_overhead_ns"], "batched_mean_ns": round(s["batched_mean_ns"], 2)}
 
 
+# ------------------------------------------------------------------ parity of the timed buffers
+def parity_windows(count, k=16, w=2048, seed=5):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    return [(0, w), (count - w - 3, count)] + [(int(s), int(s) + w) for s in rng.integers(0, count - w, k)]
+
+
+def check_parity(L, comm, bufs, host_inputs, ranks_here, n, count, step, gather):
+    """Re-fill the timed buffers with their inputs, run ONE step of the same
+    launch configuration, and compare sampled windows with the oracle (rank-
+    ordered fold, oracle/allreduce.py).  Two-shot / one-shot results must be
+    bit-exact (R2); ring / tree within 1e-6 n sum|x|.  gather(obj) -> list over
+    processes (identity for one process).  Returns the `parity` object."""
+    import numpy as np
+    import torch
+    from oracle import allreduce as orc
+    wins = parity_windows(count)
+    for b, x in zip(bufs, host_inputs):
+        b.copy_(torch.from_numpy(x))
+    torch.cuda.synchronize()
+    step()
+    torch.cuda.synchronize()
+    comm.check()
+    d = comm.last_decision()
+    exact = L.ALGO_NAMES[d.algo] in ("oneshot", "twoshot")
+    # every rank's input windows, rank order
+    mine = {r: [x[lo:hi].copy() for lo, hi in wins] for r, x in zip(ranks_here, host_inputs)}
+    allwin = {}
+    for part in gather(mine):
+        allwin.update(part)
+    ok, worst, hashes = True, 0.0, []
+    for b in bufs:
+        got = b.cpu().numpy()
+        hb = hashlib.sha1()
+        for k, (lo, hi) in enumerate(wins):
+            xs = [allwin[r][k] for r in range(n)]
+            exp = orc.allreduce(xs, "f32", "sum")
+            g = got[lo:hi]
+            hb.update(g.tobytes())
+            if exact:
+                ok = ok and bool(np.array_equal(g.view(np.uint32), exp.view(np.uint32)))
+            else:
+                bound = 1e-6 * n * np.sum(np.abs(np.stack(xs).astype(np.float64)), axis=0)
+                err = np.abs(g.astype(np.float64) - exp.astype(np.float64))
+                worst = max(worst, float(np.max(err / np.maximum(bound, 1e-300))))
+                ok = ok and bool(np.all(err <= bound))
+        hashes.append(hb.hexdigest())
+    alls = gather({"ok": ok, "hashes": hashes, "worst": worst})
+    identical = len({h for a in alls for h in a["hashes"]}) == 1
+    ok_all = all(a["ok"] for a in alls) and identical
+    return {"ok": bool(ok_all), "windows": len(wins), "elements_per_rank": sum(hi - lo for lo, hi in wins),
+            "rule": "bit-exact vs the rank-ordered oracle" if exact else "|y - y*| <= 1e-6 n sum|x| (R2)",
+            "max_err_over_bound": round(max(a["worst"] for a in alls), 6) if not exact else 0.0,
+            "ranks_identical": identical,
+            "what": "same buffers and launch configuration as the timed steps, re-filled with their inputs"}
+
+
 # ------------------------------------------------------------------ polar
 def run_polar(args):
-    import numpy as np
     import torch
 
     import synth
@@ -222,6 +312,11 @@ def run_polar(args):
     if shared:
         local = 0
     torch.cuda.set_device(local)
+    nccl_log = None
+    if real and not shared:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import nccl_ctypes
+        nccl_log = nccl_ctypes.enable_tuning_log(os.path.join(tempfile.gettempdir(), f"polar_nccl_tuning.r{rank}"))
     pg = None
     if real:
         import torch.distributed as dist
@@ -238,13 +333,18 @@ def run_polar(args):
     else:
         comm = L.Comm.virtual(VIRTUAL_RANKS, local)
         n = VIRTUAL_RANKS
+
+        def allgather(b):
+            return [b]
     if args.policy:
         with open(args.policy) as f:
             rows = [tuple(r) for r in json.load(f)["rows"]]
         L.set_policy(rows)
     count = S_BYTES // 4
-    # symmetric buffers (zero-copy): nlocal tensors
-    bufs = comm.mem_alloc_tensors(count, torch.float32)
+    max_bytes = S_BYTES if not real else (16 << 20 if shared else max(NVLINK_SIZES))
+    # symmetric buffers (zero-copy): nlocal tensors; the timed message is their first 128 MiB
+    big = comm.mem_alloc_tensors(max(count, max_bytes // 4), torch.float32)
+    bufs = [b[:count] for b in big]
     ranks_here = list(range(n)) if not real else [rank]
     host_inputs = [synth.gen("f32", count, r, cfg=2, dist="unif") for r in ranks_here]
     for b, x in zip(bufs, host_inputs):
@@ -292,6 +392,9 @@ def run_polar(args):
     t_step = max_over_ranks(ev0.elapsed_time(ev1) / 1e3 / args.steps)
     value = busbw(S_BYTES, n, t_step)
 
+    # the timed buffers, re-filled, one more step of the same configuration, checked
+    parity = check_parity(L, comm, bufs, host_inputs, ranks_here, n, count, step, allgather)
+
     # roofline of the (only) kernel of the step: the dispatched allreduce kernel
     peak, peak_src = load_peaks()
     if real:
@@ -309,26 +412,12 @@ def run_polar(args):
         roof["traffic"] = traffic.get("dram_bytes_per_launch")
         roof["traffic_source"] = traffic.get("source")
 
-    # per-size sweep (C2 sizes), policy-selected
-    sweep = {}
-    for sz in C2_SIZES:
-        cnt = sz // 4
-        it = max(5, min(50, int(0.05 / max(1e-6, t_step * sz / S_BYTES))))
-        for _ in range(3):
-            comm.allreduce_raw(ptrs, cnt, L.FLOAT32, L.SUM, sptr)
-        barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(it):
-            comm.allreduce_raw(ptrs, cnt, L.FLOAT32, L.SUM, sptr)
-        b.record(stream)
-        b.synchronize()
-        t = max_over_ranks(a.elapsed_time(b) / 1e3 / it)
-        d = comm.last_decision()
-        sweep[str(sz)] = {"busbw_gbs": round(busbw(sz, n, t), 1), "us": round(t * 1e6, 1),
-                          "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
-                          "launched_channels": comm.launched_channels()}
+    # per-size sweep
+    if real:
+        sweep = nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, allgather, shared,
+                             nccl_log)
+    else:
+        sweep = c2_sweep_virtual(L, comm, big, n, stream, t_step)
     comm.check()
 
     # e2e: through the C-ABI with HOST buffers; H2D + allreduce + D2H inside the timed region
@@ -349,6 +438,7 @@ def run_polar(args):
     e2e = {"value": round(busbw(S_BYTES, n, t_e2e), 3), "unit": "GB/s",
            "h2d_bytes_per_step": len(bufs) * S_BYTES, "d2h_bytes_per_step": len(bufs) * S_BYTES,
            "ms_per_step": round(t_e2e * 1e3, 3)}
+    e2e["pcie"] = pcie_roofline(torch, len(bufs) * S_BYTES, t_e2e, max_over_ranks)
 
     # p2p probe: the measured peer-path roofline on the same buffers
     # (after the timed regions: the probe overwrites the peer buffers)
@@ -372,7 +462,7 @@ def run_polar(args):
         # else the nominal 900 GB/s per direction.
         measured = min(probe_out["load_gbs_min_over_ranks"], probe_out["store_gbs_min_over_ranks"])
         use_probe = not shared and measured > 0
-        npeak = round(measured, 1) if use_probe else 900.0
+        npeak = round(measured, 1) if use_probe else NVLINK_GBS
         hbm_roof = roof
         roof = {"bound": "nvlink", "achieved": round(value, 1), "peak": npeak, "unit": "GB/s",
                 "frac": round(value / npeak, 4), "traffic": None,
@@ -380,10 +470,9 @@ def run_polar(args):
                                 else "nominal 900 GB/s per direction per GPU (B200 NVLink 5)"),
                 "algorithmic_bytes_per_launch": int(S_BYTES * 2 * (n - 1) / n), "kernel": hbm_roof["kernel"],
                 "note": "per-rank NVLink egress; the local-HBM view is in 'hbm'", "hbm": hbm_roof}
-
-    nccl = None
-    if real and not shared:
-        nccl = time_nccl(args, bufs[0], count, n, stream)
+        if use_probe:
+            for v in sweep["sizes"].values():
+                v["frac_of_probe"] = round(v["polar_busbw_gbs"] / npeak, 4)
 
     if rank == 0:
         cpu = cpu_baseline(n, count)
@@ -397,18 +486,22 @@ def run_polar(args):
             "decision": {"algo": L.ALGO_NAMES[decision.algo], "proto": L.PROTO_NAMES[decision.proto],
                          "nchannels": decision.nchannels, "generation": decision.generation,
                          "launched_channels": launched_nch},
+            "parity": parity,
             "algbw_gbs": round(S_BYTES / t_step / 1e9, 2),
-            "nvlink_frac": round(value / 900.0, 4) if real else None,
+            "nvlink_frac": round(value / NVLINK_GBS, 4) if real else None,
             "nvlink_frac_of_probe": (round(value / min(probe_out["load_gbs_min_over_ranks"],
                                                        probe_out["store_gbs_min_over_ranks"]), 4)
                                      if real and not shared else None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks.summary(), "c2_sweep": sweep, "decision_cost_ns": decision_cost(L),
-            "p2p_probe": probe_out,
+            "clocks": clocks.summary(), ("nvlink_sweep" if real else "c2_sweep"): sweep,
+            "decision_cost_ns": decision_cost(L), "p2p_probe": probe_out,
         }
-        if nccl:
-            out["nccl_default"] = nccl
-            out["speedup_vs_nccl"] = round(value / nccl["busbw_gbs"], 4)
+        if real and sweep.get("nccl_version"):
+            nd = sweep["sizes"].get(str(S_BYTES), {})
+            if nd.get("nccl_busbw_gbs"):
+                out["nccl_default"] = {"busbw_gbs": nd["nccl_busbw_gbs"], "us": nd["nccl_us"],
+                                       "choice": nd.get("nccl_choice"), "version": sweep["nccl_version"]}
+                out["speedup_vs_nccl"] = round(value / nd["nccl_busbw_gbs"], 4)
         print(json.dumps(out), flush=True)
     comm.destroy()
     if pg:
@@ -419,26 +512,185 @@ def kernel_name(L, d):
     return f"allreduce_kernel<f32,sum,{L.ALGO_NAMES[d.algo]},{L.PROTO_NAMES[d.proto]}>"
 
 
-def time_nccl(args, buf, count, n, stream):
-    """NCCL's default AllReduce (no NCCL_* overrides) on the same buffer."""
+def pcie_roofline(torch, nbytes, t_e2e, max_over_ranks):
+    """e2e bound: the step moves nbytes host->device and nbytes back over this
+    GPU's PCIe link; measured here with pinned copies (each direction alone, and
+    both at once on two streams) so the e2e time has its own floor."""
+    n = min(nbytes, 256 << 20)
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    t_h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    t_d2h = timed(lambda: h.copy_(d, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    t_both = timed(both)
+    h2d, d2h, bidir = n / t_h2d / 1e9, n / t_d2h / 1e9, n / t_both / 1e9
+    floor = nbytes / (bidir * 1e9)          # both directions overlapped at the measured concurrent rate
+    return {"h2d_gbs": round(h2d, 1), "d2h_gbs": round(d2h, 1), "bidir_each_gbs": round(bidir, 1),
+            "floor_ms": round(floor * 1e3, 3), "frac": round(floor / t_e2e, 4),
+            "what": "e2e floor = bytes each way / concurrent per-direction PCIe rate (pinned copies, this GPU)"}
+
+
+def _time_calls(fn, iters, stream, flush=None):
+    """Mean device time of one call: back to back between two events, or (flush
+    given) each call between its own events after an L2 flush."""
     import torch
-    import torch.distributed as dist
-    g = dist.new_group(backend="nccl")
-    t = buf[:count]
-    for _ in range(max(3, args.warmup)):
-        dist.all_reduce(t, group=g)
+    if flush is None:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / 1e3 / iters
+    tot = 0.0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in evs:
+        flush()
+        a.record(stream)
+        fn()
+        b.record(stream)
     torch.cuda.synchronize()
-    dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(torch.cuda.current_stream())
-    for _ in range(args.steps):
-        dist.all_reduce(t, group=g)
-    b.record(torch.cuda.current_stream())
-    b.synchronize()
-    x = torch.tensor([a.elapsed_time(b) / 1e3 / args.steps], dtype=torch.float64)
-    dist.all_reduce(x, op=dist.ReduceOp.MAX)
-    tt = float(x.item())
-    return {"busbw_gbs": round(busbw(count * 4, n, tt), 2), "us": round(tt * 1e6, 1)}
+    for a, b in evs:
+        tot += a.elapsed_time(b) / 1e3
+    return tot / iters
+
+
+def c2_sweep_virtual(L, comm, big, n, stream, t_step):
+    """C2 sizes (4-128 MiB per rank), policy-selected, 8 virtual ranks.  Where
+    the n ranks' buffers fit in twice the L2 (n S <= 252 MB) every call is timed
+    alone after an L2 flush (a 256 MiB write), so no point is an L2 number."""
+    import torch
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    sptr = stream.cuda_stream
+    out = {}
+    for sz in C2_SIZES:
+        cnt = sz // 4
+        ptrs = [b.data_ptr() for b in big]
+        it = max(5, min(50, int(0.05 / max(1e-6, t_step * sz / S_BYTES))))
+
+        def call():
+            st = comm.allreduce_raw(ptrs, cnt, L.FLOAT32, L.SUM, sptr)
+            if st != 0:
+                raise L.PolarError(st, "polar_allreduce_v")
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        flushed = n * sz <= 2 * L2_BYTES
+        t = _time_calls(call, it, stream, flush=(lambda: flush_buf.zero_()) if flushed else None)
+        d = comm.last_decision()
+        out[str(sz)] = {"busbw_gbs": round(busbw(sz, n, t), 1), "us": round(t * 1e6, 1),
+                        "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
+                        "launched_channels": comm.launched_channels(),
+                        "l2": "flushed before every call" if flushed else "n x S > 2 x L2, back to back"}
+    return out
+
+
+def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, allgather, shared, nccl_log):
+    """N > 1: busBW per size, 4 KiB - 1 GiB, on the same symmetric buffers and
+    stream: polar with the active table, polar with `bad_channels` (PAPER.md
+    L581: every size at 1 channel, algorithm / protocol deferred), polar with a
+    tuned table if policies/b200_nvlink<n>.json exists, and NCCL's default
+    (ctypes libnccl, no overrides; its algorithm / protocol from its TUNING
+    log).  Back-to-back calls like nccl-tests; sizes with S <= L2 are labelled."""
+    import torch
+    sptr = stream.cuda_stream
+    ptr = big[0].data_ptr()
+    sizes = [s for s in NVLINK_SIZES if s <= (16 << 20 if shared else max(NVLINK_SIZES))]
+    nccl = ncomm = None
+    version = None
+    if not shared:
+        try:
+            import nccl_ctypes
+            nccl = nccl_ctypes.Nccl()
+            version = nccl.version()
+            uid = allgather(nccl.unique_id() if rank == 0 else None)[0]
+            ncomm = nccl.init(n, uid, rank)
+        except Exception as e:  # noqa: BLE001
+            nccl, version = None, f"unavailable: {e}"
+    prev_rows, _ = L.get_policy()
+    tuned_path = os.path.join(ROOT, "policies", f"b200_nvlink{n}.json")
+    tuned = None
+    if os.path.exists(tuned_path):
+        with open(tuned_path) as f:
+            tuned = [tuple(r) for r in json.load(f)["rows"]]
+    variants = [("polar", prev_rows), ("bad_channels", [(0, 0, U64_MAX, L.UNSET, L.UNSET, 1)])]
+    if tuned:
+        variants.append(("tuned", tuned))
+
+    def polar_call(cnt):
+        st = comm.allreduce_raw([ptr], cnt, L.FLOAT32, L.SUM, sptr)
+        if st != 0:
+            raise L.PolarError(st, "polar_allreduce")
+
+    out = {}
+    for sz in sizes:
+        cnt = sz // 4
+        rec = {"l2_resident_possible": sz <= L2_BYTES}
+        for name, rows in variants:
+            L.set_policy(rows)
+            for _ in range(3):
+                polar_call(cnt)
+            torch.cuda.synchronize()
+            # the iteration count must be identical on every rank (collective calls)
+            t1 = max_over_ranks(_time_calls(lambda: polar_call(cnt), 1, stream))
+            it = int(max(5, min(200, 2e-3 / max(t1, 1e-7))))
+            barrier()
+            t = max_over_ranks(_time_calls(lambda: polar_call(cnt), it, stream))
+            d = comm.last_decision()
+            rec[f"{name}_busbw_gbs"] = round(busbw(sz, n, t), 2)
+            rec[f"{name}_us"] = round(t * 1e6, 2)
+            rec[f"{name}_decision"] = [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels]
+        L.set_policy(prev_rows)
+        if nccl is not None:
+            def nccl_call():
+                nccl.allreduce(ncomm, ptr, cnt, 7, sptr)
+            for _ in range(3):
+                nccl_call()
+            torch.cuda.synchronize()
+            t1 = max_over_ranks(_time_calls(nccl_call, 1, stream))
+            it = int(max(5, min(200, 2e-3 / max(t1, 1e-7))))
+            barrier()
+            t = max_over_ranks(_time_calls(nccl_call, it, stream))
+            rec["nccl_busbw_gbs"] = round(busbw(sz, n, t), 2)
+            rec["nccl_us"] = round(t * 1e6, 2)
+            rec["speedup_vs_nccl"] = round(rec["polar_busbw_gbs"] / rec["nccl_busbw_gbs"], 4)
+        rec["nvlink_frac"] = round(rec["polar_busbw_gbs"] / NVLINK_GBS, 4)
+        out[str(sz)] = rec
+    comm.check()
+    if nccl is not None:
+        torch.cuda.synchronize()
+        choices = nccl_ctypes.parse_tuning(nccl_log) if nccl_log else {}
+        for sz in sizes:
+            if sz in choices:
+                out[str(sz)]["nccl_choice"] = list(choices[sz])
+        nccl.destroy(ncomm)
+    # the paper's E10 (best single global choice) needs the full grid: scripts/tune_policy.py --real
+    best = None
+    if out:
+        wins = [s for s, r in out.items() if "speedup_vs_nccl" in r and r["speedup_vs_nccl"] > 1.0
+                and (4 << 20) <= int(s) <= (128 << 20)]
+        best = {"beats_nccl_in_4_128MiB_at": wins}
+    return {"sizes": out, "nccl_version": version, "summary": best,
+            "variants": [v[0] for v in variants] + (["nccl_default"] if nccl is not None else [])}
 
 
 def main():

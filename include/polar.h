@@ -22,10 +22,17 @@
  *     comm and returned by the NEXT call on it, or by polar_comm_check().
  *   - Cross-rank consistency (the paper is silent, DESIGN.md
  *     R12): on a real comm every launch carries a decision tag (kind, algorithm,
- *     protocol, channels, dtype, op, count, root).  Each rank publishes its tag
- *     in its scratch and compares its peers' tags of the PREVIOUS launch; a
- *     difference (a policy swapped on one rank only, mismatched counts or ops)
- *     latches POLAR_ESTATE, one launch late, instead of going unnoticed.
+ *     protocol, channels, dtype, op, count, root, and for zero-copy kernels the
+ *     buffer path: registration id + offset, or the bounce region).
+ *       * Kernels with an entry handshake (two-shot Simple, ReduceScatter,
+ *         AllGather, Broadcast) exchange the tag inside it: ranks that disagree
+ *         latch POLAR_ESTATE and leave BEFORE any data moves (synchronous).
+ *       * Every other kernel publishes its tag in its scratch and compares its
+ *         peers' tags of the PREVIOUS launch: a difference latches POLAR_ESTATE
+ *         one launch late; the mismatched call's output is undefined, and the
+ *         last call of a sequence is only checked by a following launch.
+ *     Ranks that pick different kernels altogether (a policy swapped on one
+ *     rank only) usually wait for each other in vain: POLAR_ETIMEOUT.
  */
 #ifndef POLAR_H
 #define POLAR_H
@@ -121,8 +128,13 @@ typedef struct polar_comm_s* polar_comm_t;   /* opaque; owned by the library */
  * compare-and-swap on the pointer").  The rows are COPIED.
  * Validation: nrows <= 64; known enums; nranks <= 8; only known flag bits; rows of one
  * (coll, nranks) group strictly ascending in max_bytes -> else POLAR_EINVAL;
- * NVLS -> POLAR_EUNSUPPORTED (LL128 is accepted: every algorithm has an LL128
- * kernel).  On any rejection the active policy and
+ * a decision no kernel implements -> POLAR_EUNSUPPORTED: NVLS while no comm of
+ * this process holds a multicast object (polar_nvls_available), and
+ * ReduceScatter / AllGather / Broadcast rows naming anything but ONESHOT /
+ * SIMPLE (or UNSET).  LL128 is accepted (every AllReduce algorithm has an
+ * LL128 kernel; real comms refuse it at call time
+ * until the line-atomicity probe passed over their transport, see
+ * polar_allreduce).  On any rejection the active policy and
  * its generation are unchanged ("the old policy continues").
  * nrows == 0 installs the empty policy (the paper's `noop`, L433).
  * On success the generation increases by exactly 1 and is stored in
@@ -227,8 +239,18 @@ polar_status polar_mem_free(polar_comm_t comm, void* ptr);
 
 /* Register caller-owned device memory [buf, buf+bytes) for zero-copy use
  * (collective; every rank registers its own buffer in the same call order).
- * Virtual comms accept and ignore it (all ranks are local). */
+ * Virtual comms accept and ignore it (all ranks are local).  A registration
+ * remembers its allocation (CU_POINTER_ATTRIBUTE_BUFFER_ID): once that
+ * allocation is freed (cudaFree; a caching allocator that keeps the segment
+ * does not free it) the registration is stale and is dropped at its next use,
+ * and the call takes the unregistered path — if another rank still uses its
+ * registration for the same call, the entry handshake latches POLAR_ESTATE. */
 polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes);
+
+/* Drop the registration whose start is `buf` (collective: synchronises the
+ * device, host-barriers, closes the peers' IPC mappings no other registration
+ * uses).  POLAR_OK also when `buf` is not (or no longer) registered. */
+polar_status polar_deregister(polar_comm_t comm, void* buf);
 
 /* ----------------------------------------------------------------- AllReduce */
 

@@ -102,8 +102,12 @@ def validate(rows) -> str:
 
     "ok", or "einval" (malformed: too many rows, unknown enum, nranks > 8,
     rows of one (coll, nranks) group not strictly ascending in max_bytes), or
-    "eunsupported" (well-formed but names NVLS, not built yet).  LL128 is
-    accepted: the protocol exists.
+    "eunsupported" (well-formed but names a decision no kernel implements:
+    NVLS without a multicast object — none can be created on the 1-GPU pool,
+    DESIGN.md §1 f1 — or a ReduceScatter / AllGather / Broadcast row naming
+    anything but ONESHOT / SIMPLE, the only kernel those collectives have,
+    DESIGN.md §4).  LL128 is accepted: the protocol exists (SURVEY.md §8(f) f2;
+    PAPER.md L111, L569-571).
     """
     if len(rows) > MAXROWS:
         return "einval"
@@ -129,5 +133,7 @@ def validate(rows) -> str:
             return "einval"
         last[key] = max_bytes
         if algo == NVLS:
+            unsupported = True
+        if coll != COLL_ALLREDUCE and (algo not in (ONESHOT, UNSET) or proto not in (SIMPLE, UNSET)):
             unsupported = True
     return "eunsupported" if unsupported else "ok"

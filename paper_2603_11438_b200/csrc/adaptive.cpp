@@ -27,6 +27,7 @@ void adaptive_reset(Adaptive& a, const polar_adaptive_params& p) {
     a.win_sum = 0.0;
     a.win_cnt = 0;
     a.calls = 0;
+    a.cap = POLAR_MAXCH;
 }
 
 polar_status adaptive_validate(const polar_adaptive_params& p) {

@@ -89,7 +89,10 @@ struct Registration {
     char* base;            // local device pointer
     size_t bytes;
     char* peer[kMaxRanks]; // rank p's registered base as mapped here
+    char* peer_base[kMaxRanks];   // the IPC mapping (peer allocation start) behind peer[p]
     bool owned;            // allocated by polar_mem_alloc
+    uint32_t id;           // registration sequence number (identical on every rank: collective)
+    unsigned long long buffer_id;  // CU_POINTER_ATTRIBUTE_BUFFER_ID of the allocation at registration
 };
 
 struct polar_comm_s {
@@ -99,6 +102,8 @@ struct polar_comm_s {
     char* scratch_own[kMaxRanks] = {};   // allocations owned by this process
     char* scratch[kMaxRanks] = {};       // rank p's scratch as addressable here
     std::vector<Registration> regs;
+    uint32_t reg_seq = 0;                // registrations made (collective, so equal on every rank)
+    uint64_t stale_regs = 0;             // user registrations dropped because their allocation was freed
     std::vector<char*> ipc_mapped;       // to close at destroy
     struct Opened { int peer; cudaIpcMemHandle_t h; char* base; };
     std::vector<Opened> opened;          // IPC handles already opened (one open per allocation)
@@ -203,10 +208,17 @@ polar_status check_latched(polar_comm_s* c) {
 
 // Decision tag of one launch (SURVEY.md §8(b) "cross-rank consistency"): every
 // field that must agree across ranks for the exchange to be correct.
-uint64_t decision_tag(int kind, int algo, int proto, int nch, int dtype, int op, uint64_t count, int root) {
+// `path` identifies how the buffers are addressed (zero-copy registration id
+// and offset, bounce, staged), so that ranks which took different paths for one
+// call disagree in the tag.
+constexpr uint64_t kPathBounce = 0xB0B0ull;   // two-shot through the scratch bounce region
+
+uint64_t decision_tag(int kind, int algo, int proto, int nch, int dtype, int op, uint64_t count, int root,
+                      uint64_t path = 0) {
     uint64_t h = ((uint64_t)kind) | ((uint64_t)algo << 4) | ((uint64_t)proto << 8) | ((uint64_t)nch << 12) |
                  ((uint64_t)dtype << 20) | ((uint64_t)op << 26) | ((uint64_t)(root & 0xff) << 30);
     h ^= count * 0x9E3779B97F4A7C15ull;
+    h ^= (path + 0x632BE59BD9B4E019ull) * 0xD6E8FEB86659FD93ull;
     h ^= h >> 31; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 29;
     return h | 1;   // never 0
 }
@@ -312,10 +324,66 @@ polar_status alloc_common(polar_comm_s* c) {
     return POLAR_OK;
 }
 
-// find a registration containing [p, p+bytes)
-const Registration* find_reg(const polar_comm_s* c, const char* p, size_t bytes) {
-    for (const auto& r : c->regs)
-        if (p >= r.base && p + bytes <= r.base + r.bytes) return &r;
+// Driver entry points through the runtime (no -lcuda link).
+template <class F> F driver_fn(const char* name) {
+    cudaDriverEntryPointQueryResult q;
+    void* fp = nullptr;
+    if (cudaGetDriverEntryPoint(name, &fp, cudaEnableDefault, &q) != cudaSuccess || !fp) return nullptr;
+    return reinterpret_cast<F>(fp);
+}
+
+// Drop registration i: close every peer IPC mapping no other registration uses
+// (a peer allocation may back several registrations: caching allocators).
+void release_registration(polar_comm_s* c, size_t i) {
+    const Registration r = c->regs[i];
+    c->regs.erase(c->regs.begin() + (long)i);
+    for (int p = 0; p < c->nranks; ++p) {
+        char* b = r.peer_base[p];
+        if (p == c->rank0 || !b) continue;
+        bool used = false;
+        for (const auto& o : c->regs) used = used || o.peer_base[p] == b;
+        if (used) continue;
+        for (size_t k = 0; k < c->opened.size(); ++k)
+            if (c->opened[k].peer == p && c->opened[k].base == b) {
+                cudaIpcCloseMemHandle(b);
+                c->opened.erase(c->opened.begin() + (long)k);
+                break;
+            }
+        for (size_t m = 0; m < c->ipc_mapped.size(); ++m)
+            if (c->ipc_mapped[m] == b) {
+                c->ipc_mapped.erase(c->ipc_mapped.begin() + (long)m);
+                break;
+            }
+    }
+}
+
+// Unique id of the allocation containing p (never reused within a process:
+// CU_POINTER_ATTRIBUTE_BUFFER_ID), 0 if unknown.
+unsigned long long buffer_id_of(const void* p) {
+    using Fn = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+    static Fn get = driver_fn<Fn>("cuPointerGetAttribute");
+    unsigned long long id = 0;
+    if (!get || get(&id, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)p) != CUDA_SUCCESS) return 0;
+    return id;
+}
+
+// find a registration containing [p, p+bytes).  A user registration whose
+// allocation was freed since (a caching allocator may hand the same addresses
+// to a new allocation, which peers' IPC mappings do not show) is stale: it is
+// dropped here, and the call takes the path of an unregistered buffer.  The
+// decision tag carries the path and the registration id, so ranks that disagree
+// are caught by the entry handshake before any data moves.
+const Registration* find_reg(polar_comm_s* c, const char* p, size_t bytes) {
+    for (size_t i = 0; i < c->regs.size(); ++i) {
+        const Registration& r = c->regs[i];
+        if (!(p >= r.base && p + bytes <= r.base + r.bytes)) continue;
+        if (!r.owned && r.buffer_id && buffer_id_of(p) != r.buffer_id) {
+            release_registration(c, i);   // local: closes this rank's mappings of the peers' buffers
+            c->stale_regs++;
+            return nullptr;
+        }
+        return &c->regs[i];
+    }
     return nullptr;
 }
 
@@ -350,7 +418,7 @@ void destroy_comm(polar_comm_s* c, bool collective) {
 }
 
 // Exchange IPC handles of `base` (allocation start) + offset; fill peer[] pointers.
-polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks]) {
+polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks], char* peer_base[kMaxRanks] = nullptr) {
     struct Msg { cudaIpcMemHandle_t h; unsigned long long off; int pid_ok; };
     CUdeviceptr base = 0;
     size_t sz = 0;
@@ -371,6 +439,7 @@ polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks])
     std::vector<Msg> all(c->nranks);
     if (c->ag(&mine, all.data(), sizeof(Msg), c->user) != 0) return POLAR_ESTATE;
     for (int p = 0; p < c->nranks; ++p) {
+        if (peer_base) peer_base[p] = nullptr;
         if (p == c->rank0) { peer[p] = ptr; continue; }
         // a peer allocation may back several registrations (caching allocators):
         // open each IPC handle once and reuse the mapping
@@ -386,6 +455,7 @@ polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks])
             c->opened.push_back({p, all[p].h, base_p});
         }
         peer[p] = base_p + all[p].off;
+        if (peer_base) peer_base[p] = base_p;
     }
     return POLAR_OK;
 }
@@ -492,10 +562,18 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     const void* fn = kernel_for(dtype, op, (int)d.algo, (int)d.proto);
     if (!fn) return POLAR_EUNSUPPORTED;
     c->last = d;                      // the policy's decision (what the hook returned)
-    if ((d.flags & POLAR_ROW_ADAPTIVE_NCH) && count > 0 && c->nranks > 1) {
-        // closed loop: the row's nchannels is the cap, the controller picks c
-        st = adaptive_tick(c, d.nchannels);
+    const bool adaptive_row = (d.flags & POLAR_ROW_ADAPTIVE_NCH) && count > 0 && c->nranks > 1;
+    if (c->ad.prm.enabled && count > 0 && c->nranks > 1) {
+        // The window schedule counts every AllReduce of the comm while the loop is
+        // enabled (polar_adaptive_config is collective), never the local policy:
+        // a rank whose table differs cannot leave its peers blocked in the
+        // window all-gather of a real comm.  The cap is the last adaptive row's.
+        if (adaptive_row) c->ad.cap = d.nchannels;
+        st = adaptive_tick(c, c->ad.cap);
         if (st != POLAR_OK) return st;
+    }
+    if (adaptive_row) {
+        // closed loop: the row's nchannels is the cap, the controller picks c
         d.nchannels = c->ad.c < d.nchannels ? c->ad.c : d.nchannels;
     }
     if (c->is_virtual) {
@@ -512,9 +590,10 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     P.nch = (int)d.nchannels;
     const int grid = c->nlocal * P.nch;
     // the bounce path launches per chunk: each launch's count is in its own tag
-    auto tag_for = [&](size_t cnt) { return decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, cnt, 0); };
-    P.dtag = tag_for(count);
-    if (c->ad.prm.enabled) {
+    P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0);
+    if (c->ad.prm.enabled && adaptive_row) {
+        // telemetry from adaptive-row launches only: a window's mean never mixes
+        // in the latencies of other sizes or algorithms
         adaptive_drain(c);           // keep the ring from lapping between windows
         P.tel = c->tel_dev;
         P.seq = ++c->tel_seq;
@@ -554,6 +633,9 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         }
         P.vec = vec;
         P.count = count;
+        // zero-copy: every rank must address the same registration at the same offset
+        P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0,
+                              ((uint64_t)(reg->id + 1) << 40) ^ (uint64_t)off);
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
     // unregistered: bounce through the symmetric scratch, chunk by chunk
@@ -565,7 +647,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         char* src = mine + done * es;
         CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, stream));
         P.count = n;
-        P.dtag = tag_for(n);
+        P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, n, 0, kPathBounce);
         st = launch_kernel(c, fn, P, grid, stream, smem);
         if (st != POLAR_OK) return st;
         CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, stream));
@@ -636,6 +718,8 @@ polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* cons
         const Registration* reg = find_reg(c, shared, ext);
         if (!reg) return POLAR_EINVAL;
         const size_t off = (size_t)(shared - reg->base);
+        P.dtag = decision_tag(1 + mode, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, root,
+                              ((uint64_t)(reg->id + 1) << 40) ^ (uint64_t)off);
         for (int p = 0; p < c->nranks; ++p) {
             char* peer = reg->peer[p] + off;
             if (mode == 1) {
@@ -786,7 +870,9 @@ polar_status polar_mem_alloc(polar_comm_t comm, size_t bytes, void** ptrs) {
     if (cudaMalloc(reinterpret_cast<void**>(&r.base), bytes) != cudaSuccess) return POLAR_ENOMEM;
     r.bytes = bytes;
     r.owned = true;
-    polar_status st = exchange_and_map(comm, r.base, r.peer);
+    r.id = comm->reg_seq++;
+    r.buffer_id = buffer_id_of(r.base);
+    polar_status st = exchange_and_map(comm, r.base, r.peer, r.peer_base);
     if (st != POLAR_OK) { cudaFree(r.base); return st; }
     comm->regs.push_back(r);
     ptrs[0] = r.base;
@@ -810,24 +896,9 @@ polar_status polar_mem_free(polar_comm_t comm, void* ptr) {
             // peers' copies (each owned buffer is its own allocation, mapped at
             // offset 0), everyone has unmapped, then each rank frees its own
             polar_status st = host_barrier(comm);
-            const Registration r = comm->regs[i];
-            for (int p = 0; p < comm->nranks; ++p) {
-                if (p == comm->rank0) continue;
-                for (size_t k = 0; k < comm->opened.size(); ++k)
-                    if (comm->opened[k].peer == p && comm->opened[k].base == r.peer[p]) {
-                        cudaIpcCloseMemHandle(r.peer[p]);
-                        comm->opened.erase(comm->opened.begin() + (long)k);
-                        for (size_t m = 0; m < comm->ipc_mapped.size(); ++m)
-                            if (comm->ipc_mapped[m] == r.peer[p]) {
-                                comm->ipc_mapped.erase(comm->ipc_mapped.begin() + (long)m);
-                                break;
-                            }
-                        break;
-                    }
-            }
+            release_registration(comm, i);
             if (st == POLAR_OK) st = host_barrier(comm);
             cudaFree(ptr);
-            comm->regs.erase(comm->regs.begin() + (long)i);
             return st;
         }
     return POLAR_EINVAL;
@@ -843,10 +914,29 @@ polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes) {
     r.base = reinterpret_cast<char*>(buf);
     r.bytes = bytes;
     r.owned = false;
-    polar_status st = exchange_and_map(comm, r.base, r.peer);
+    r.id = comm->reg_seq++;
+    r.buffer_id = buffer_id_of(buf);
+    polar_status st = exchange_and_map(comm, r.base, r.peer, r.peer_base);
     if (st != POLAR_OK) return st;
     comm->regs.push_back(r);
     return POLAR_OK;
+}
+
+polar_status polar_deregister(polar_comm_t comm, void* buf) {
+    if (!comm || !buf) return POLAR_EINVAL;
+    if (comm->is_virtual) return POLAR_OK;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
+    cudaDeviceSynchronize();
+    polar_status st = host_barrier(comm);   // no peer still reads or writes through the mappings
+    for (size_t i = 0; i < comm->regs.size(); ++i)
+        if (comm->regs[i].base == buf && !comm->regs[i].owned) {
+            release_registration(comm, i);
+            break;
+        }
+    // (not registered here, or already dropped as stale: still collective, still OK)
+    return st;
 }
 
 polar_status polar_allreduce(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, polar_op op,

@@ -93,11 +93,27 @@ __device__ __forceinline__ void geo_slice(const Geo& g, unsigned long long NP, u
 #ifndef POLAR_VIRTUAL_HANDSHAKE
 #define POLAR_VIRTUAL_HANDSHAKE 0
 #endif
+// The entry handshake also carries the launch's decision tag (F_ENTRY_SIG,
+// written before the release of F_ENTRY): a rank whose peers addressed this
+// call differently (another registration or offset, the bounce path, another
+// count / op / dtype / channel count) sees a foreign tag right after the
+// barrier, latches POLAR_ESTATE and leaves before any data moves — every rank
+// sees the difference (it is symmetric), so all of them leave and none waits.
 __device__ __forceinline__ bool handshake_entry(const Params& P, const Who& w, uint64_t e) {
     if (!P.sys && !POLAR_VIRTUAL_HANDSHAKE) return true;
-    if (w.tid < w.n) jitter(P), st_release(flag_ptr(P, w.tid, F_ENTRY, w.c, w.r), e, P.sys);
+    if (w.tid < w.n) {
+        jitter(P);
+        if (P.sys) st_relaxed(flag_ptr(P, w.tid, F_ENTRY_SIG, w.c, w.r), P.dtag, P.sys);
+        st_release(flag_ptr(P, w.tid, F_ENTRY, w.c, w.r), e, P.sys);
+    }
     bool ok = true;
-    if (w.tid < w.n) ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, w.tid), e);
+    if (w.tid < w.n) {
+        ok = wait_geq(P, flag_ptr(P, w.r, F_ENTRY, w.c, w.tid), e);
+        if (ok && P.sys && *(volatile const uint64_t*)flag_ptr(P, w.r, F_ENTRY_SIG, w.c, w.tid) != P.dtag) {
+            raise_error(P, POLAR_ESTATE);
+            ok = false;
+        }
+    }
     return __syncthreads_and(ok) != 0;
 }
 __device__ __forceinline__ bool handshake_exit(const Params& P, const Who& w, uint64_t e) {

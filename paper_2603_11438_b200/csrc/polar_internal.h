@@ -33,7 +33,8 @@ enum FlagKind : int {
     F_PROBE_ENTRY = 10,  // p2p probe: entry barrier (slot = source rank)
     F_PROBE_EXIT = 11,   // p2p probe: exit barrier
     F_PROBE_PP = 12,     // p2p probe: ping-pong flag (channel 0, slot 0)
-    F_NKINDS = 13
+    F_ENTRY_SIG = 13,    // zero-copy kernels: the decision tag of the launch behind F_ENTRY
+    F_NKINDS = 14
 };
 constexpr size_t kFlagRow = 128;  // bytes per (kind, channel) row
 constexpr size_t kFlagBytes = (size_t)F_NKINDS * kMaxCh * kFlagRow;
@@ -87,7 +88,8 @@ struct Adaptive {
     double ref[POLAR_MAXCH + 1] = {};   // last non-contended window mean per channel count (0 = unknown)
     double win_sum = 0.0;         // samples of the open window
     uint64_t win_cnt = 0;
-    uint64_t calls = 0;           // adaptive calls seen (window boundary every prm.period)
+    uint64_t calls = 0;           // calls seen while enabled (window boundary every prm.period)
+    uint32_t cap = POLAR_MAXCH;   // nchannels of the last adaptive row (the controller's cap)
 };
 void adaptive_reset(Adaptive& a, const polar_adaptive_params& p);
 polar_status adaptive_validate(const polar_adaptive_params& p);

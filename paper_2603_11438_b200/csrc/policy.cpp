@@ -74,6 +74,13 @@ polar_status validate_rows(const polar_policy_row* rows, uint32_t nrows) {
             case POLAR_PROTO_LL: case POLAR_PROTO_LL128: case POLAR_PROTO_SIMPLE: case POLAR_UNSET: break;
             default: return POLAR_EINVAL;
         }
+        // ReduceScatter / AllGather / Broadcast have one kernel: the direct
+        // all-to-all step (ONESHOT / SIMPLE); any other choice would only fail
+        // with EUNSUPPORTED at call time, so the table is refused now
+        if (r.coll != POLAR_COLL_ALLREDUCE &&
+            ((r.algo != POLAR_UNSET && r.algo != POLAR_ALGO_ONESHOT) ||
+             (r.proto != POLAR_UNSET && r.proto != POLAR_PROTO_SIMPLE)))
+            unsupported = true;
         // strictly ascending max_bytes within the (coll, nranks) group
         for (uint32_t j = 0; j < i; ++j) {
             if (rows[j].coll == r.coll && rows[j].nranks == r.nranks && r.max_bytes <= rows[j].max_bytes)

@@ -112,6 +112,7 @@ _sigs = {
     "polar_mem_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
     "polar_mem_free": (C.c_int, [_P, _P]),
     "polar_register": (C.c_int, [_P, _P, C.c_size_t]),
+    "polar_deregister": (C.c_int, [_P, _P]),
     "polar_allreduce": (C.c_int, [_P, _P, C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_allreduce_v": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_allreduce_forced": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, C.POINTER(Decision), _P]),
@@ -244,6 +245,15 @@ def _torch_dtype_code(t):
     return m[t.dtype]
 
 
+def _check_tensor(t, what, cuda=True):
+    if not hasattr(t, "data_ptr") or not hasattr(t, "is_contiguous"):
+        raise PolarError(EINVAL, f"{what}: expected a torch tensor, got {type(t).__name__}")
+    if t.is_cuda != cuda:
+        raise PolarError(EINVAL, f"{what}: expected a {'CUDA' if cuda else 'host'} tensor")
+    if not t.is_contiguous():
+        raise PolarError(EINVAL, f"{what}: tensor must be contiguous (a strided view would be read past its end)")
+
+
 def _stream_ptr(stream):
     if stream is None:
         import torch
@@ -336,14 +346,33 @@ class Comm:
         _check(lib.polar_mem_free(self.h, C.c_void_p(ptr)), "polar_mem_free")
 
     def register(self, tensor):
+        _check_tensor(tensor, "polar_register")
         _check(lib.polar_register(self.h, C.c_void_p(tensor.data_ptr()), tensor.numel() * tensor.element_size()),
                "polar_register")
 
-    def _bufs(self, tensors):
+    def deregister(self, tensor_or_ptr):
+        """Collective: drop the registration starting at this tensor's (or raw pointer's) address."""
+        ptr = tensor_or_ptr if isinstance(tensor_or_ptr, int) else tensor_or_ptr.data_ptr()
+        _check(lib.polar_deregister(self.h, C.c_void_p(ptr)), "polar_deregister")
+
+    def _list(self, tensors, what, cuda=True):
+        """nlocal tensors, each a contiguous CUDA tensor, all of one dtype and numel:
+        the C ABI sees only a pointer and one count, so a strided view or a
+        shorter tensor would make a kernel read or write past its end."""
         if not isinstance(tensors, (list, tuple)):
             tensors = [tensors]
         if len(tensors) != self.nlocal:
-            raise PolarError(EINVAL, f"need {self.nlocal} buffers, got {len(tensors)}")
+            raise PolarError(EINVAL, f"{what}: need {self.nlocal} buffers, got {len(tensors)}")
+        t0 = tensors[0]
+        for t in tensors:
+            _check_tensor(t, what, cuda)
+            if t.dtype != t0.dtype or t.numel() != t0.numel():
+                raise PolarError(EINVAL, f"{what}: every buffer must have the dtype and numel of the first "
+                                         f"({t0.dtype}, {t0.numel()}), got ({t.dtype}, {t.numel()})")
+        return list(tensors)
+
+    def _bufs(self, tensors, what="allreduce", cuda=True):
+        tensors = self._list(tensors, what, cuda)
         arr = (C.c_void_p * self.nlocal)(*[t.data_ptr() for t in tensors])
         t0 = tensors[0]
         return arr, t0.numel(), _torch_dtype_code(t0)
@@ -364,35 +393,41 @@ class Comm:
         _check(lib.polar_allreduce_forced(self.h, arr, n, dt, OP_CODES[op], C.byref(d), _stream_ptr(stream)),
                "polar_allreduce_forced")
 
-    def _ptrs(self, tensors):
-        if not isinstance(tensors, (list, tuple)):
-            tensors = [tensors]
-        if len(tensors) != self.nlocal:
-            raise PolarError(EINVAL, f"need {self.nlocal} buffers, got {len(tensors)}")
+    def _ptrs(self, tensors, what):
+        tensors = self._list(tensors, what)
         return (C.c_void_p * self.nlocal)(*[t.data_ptr() for t in tensors]), tensors[0]
+
+    def _ratio(self, big, small, what):
+        if big.dtype != small.dtype or big.numel() != self.nranks * small.numel():
+            raise PolarError(EINVAL, f"{what}: need numel {self.nranks} x {small.numel()} = "
+                                     f"{self.nranks * small.numel()} of {small.dtype}, got {big.numel()} of {big.dtype}")
 
     def reduce_scatter(self, sends, recvs, op="sum", stream=None):
         """recv_r = block r of the rank-ordered reduction of the sends (numel(send) = n * numel(recv))."""
-        s, s0 = self._ptrs(sends)
-        r, r0 = self._ptrs(recvs)
+        s, s0 = self._ptrs(sends, "reduce_scatter send")
+        r, r0 = self._ptrs(recvs, "reduce_scatter recv")
+        self._ratio(s0, r0, "reduce_scatter")
         _check(lib.polar_reduce_scatter_v(self.h, s, r, r0.numel(), _torch_dtype_code(r0), OP_CODES[op],
                                           _stream_ptr(stream)), "polar_reduce_scatter_v")
 
     def all_gather(self, sends, recvs, stream=None):
         """recv = concatenation of every rank's send (numel(recv) = n * numel(send))."""
-        s, s0 = self._ptrs(sends)
-        r, _ = self._ptrs(recvs)
+        s, s0 = self._ptrs(sends, "all_gather send")
+        r, r0 = self._ptrs(recvs, "all_gather recv")
+        self._ratio(r0, s0, "all_gather")
         _check(lib.polar_all_gather_v(self.h, s, r, s0.numel(), _torch_dtype_code(s0), _stream_ptr(stream)),
                "polar_all_gather_v")
 
     def broadcast(self, bufs, root=0, stream=None):
-        b, b0 = self._ptrs(bufs)
+        b, b0 = self._ptrs(bufs, "broadcast")
         _check(lib.polar_broadcast_v(self.h, b, b0.numel(), _torch_dtype_code(b0), int(root), _stream_ptr(stream)),
                "polar_broadcast_v")
 
     def allreduce_host(self, host_tensors, dev_tensors, op="sum", stream=None):
-        harr, n, dt = self._bufs(host_tensors)
-        darr, _, _ = self._bufs(dev_tensors)
+        harr, n, dt = self._bufs(host_tensors, "allreduce_host host", cuda=False)
+        darr, n2, dt2 = self._bufs(dev_tensors, "allreduce_host device")
+        if (n2, dt2) != (n, dt):
+            raise PolarError(EINVAL, "allreduce_host: host and device buffers differ in numel or dtype")
         _check(lib.polar_allreduce_host(self.h, harr, darr, n, dt, OP_CODES[op], _stream_ptr(stream)),
                "polar_allreduce_host")
 

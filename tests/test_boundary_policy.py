@@ -202,3 +202,21 @@ def test_committed_policy_files_validate():
         assert exp == "ok", name
         if exp == "ok":
             _compare(rows)
+
+
+def test_collective_rows_without_kernel_rejected():
+    """ReduceScatter / AllGather / Broadcast have one kernel (the direct step,
+    ONESHOT / SIMPLE): a row naming anything else is refused at install time,
+    the old table stays (VERDICT r01 weak #8), and the oracle agrees."""
+    L.set_policy([])
+    for coll in (OP.COLL_ALLGATHER, OP.COLL_BROADCAST, OP.COLL_REDUCESCATTER):
+        g0 = L.generation()
+        for algo, proto in ((OP.RING, OP.SIMPLE), (OP.TWOSHOT, OP.UNSET), (OP.UNSET, OP.LL), (OP.ONESHOT, OP.LL128)):
+            rows = [(coll, 0, 1 << 20, algo, proto, 4)]
+            st, _ = L.set_policy_status(rows)
+            assert L.STATUS_NAMES[st] == OP.validate(rows) == "eunsupported", (coll, algo, proto)
+            assert L.generation() == g0
+        ok_rows = [(coll, 0, 1 << 20, OP.ONESHOT, OP.UNSET, 4), (coll, 0, 1 << 30, OP.UNSET, OP.SIMPLE, 0)]
+        st, _ = L.set_policy_status(ok_rows)
+        assert L.STATUS_NAMES[st] == OP.validate(ok_rows) == "ok"
+    L.set_policy([])

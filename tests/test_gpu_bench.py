@@ -49,3 +49,29 @@ def test_bench_torchrun_two_ranks_shared_gpu():
     assert d["decision"]["algo"] == "twoshot"
     assert d["roofline"]["bound"] == "nvlink" and d["roofline"]["hbm"]["bound"] == "hbm"
     assert d["e2e"]["h2d_bytes_per_step"] == d["config"]["bytes_per_rank"]
+    # the timed buffers were re-filled and checked against the oracle
+    assert d["parity"]["ok"] and d["parity"]["ranks_identical"], d["parity"]
+    # N > 1 sweep schema (NCCL cleanly skipped on a shared GPU)
+    sw = d["nvlink_sweep"]
+    assert "nccl_default" not in sw["variants"] and "bad_channels" in sw["variants"]
+    assert str(4 << 10) in sw["sizes"] and str(16 << 20) in sw["sizes"]
+    for rec in sw["sizes"].values():
+        assert rec["polar_busbw_gbs"] > 0 and rec["bad_channels_decision"][2] == 1
+        assert "nccl_busbw_gbs" not in rec and 0 < rec["nvlink_frac"]
+    assert "speedup_vs_nccl" not in d and "cpu_model" in d["cpu_baseline"]
+    assert d["e2e"]["pcie"]["floor_ms"] > 0
+
+
+def test_bench_single_gpu_line():
+    """N = 1 (the driver's default run): the line carries parity, the L2-labelled
+    C2 sweep, the PCIe-bounded e2e and the CPU model."""
+    env = dict(os.environ, POLAR_TIMEOUT_MS="20000")
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    d = _line(r.stdout)
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["parity"]["ok"] and d["parity"]["ranks_identical"]
+    assert d["roofline"]["bound"] == "hbm" and d["gpu_launches"] == 5
+    for sz, rec in d["c2_sweep"].items():
+        assert rec["l2"].startswith("flushed") == (8 * int(sz) <= 2 * (126 << 20))

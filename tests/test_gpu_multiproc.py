@@ -49,3 +49,31 @@ def test_multiprocess_ipc_all_algorithms(tmp_path, nranks, tma, jitter):
     bad = [x for x in res if not (x["ok"] and x["identical"])]
     assert not bad, bad
     assert len(res) == nranks * (4 * 3 * 3 + 3 + 4 + 1 + 1 + 6 + 3 * 4 + 1)
+
+
+def test_multiprocess_north_star_size_c2(tmp_path):
+    """the north_star call at its own size — polar_allreduce on
+    128 MiB f32 per rank (C2's largest), 3 processes on CUDA IPC: registered
+    (zero-copy two-shot) and unregistered (bounce) buffers under the default
+    table, forced ring / tree Simple at 32 channels, back-to-back mixes, a
+    stale (freed) registration, deregistration, and a path mismatch that must
+    latch ESTATE before any data moves (tests/mp_worker_c2.py)."""
+    out = tmp_path / "c2.json"
+    env = dict(os.environ)
+    env.setdefault("POLAR_TIMEOUT_MS", "120000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "tests", "mp_worker_c2.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-4000:]
+    res = json.loads(out.read_text())
+    bad = [x for x in res if not (x["ok"] and x["identical"])]
+    assert not bad, bad
+    tags = {x["tag"] for x in res}
+    assert {"c2/registered/policy", "c2/unregistered/policy", "c2/ring/simple/32ch", "c2/tree/simple/32ch",
+            "c2/after-free", "c2/deregistered", "path-mismatch-latched-before-data"} <= tags
+    dec = {x["tag"]: x["decision"] for x in res if "decision" in x}
+    assert dec["c2/registered/policy"][:2] == ["twoshot", "simple"]
+    assert dec["c2/unregistered/policy"][:2] == ["twoshot", "simple"]
+    # R2 headroom of the f32 ring / tree results (reported, asserted <= 1 above)
+    print({x["tag"]: round(x["max_err_over_bound"], 4) for x in res if x["rank"] == 0 and "max_err_over_bound" in x})
