@@ -66,7 +66,7 @@ typedef enum { POLAR_SUM = 0, POLAR_MAX = 2, POLAR_MIN = 3 } polar_op;
  * all-to-all algorithms this library adds. */
 enum { POLAR_COLL_ALLREDUCE = 0, POLAR_COLL_ALLGATHER = 1, POLAR_COLL_BROADCAST = 2,
        POLAR_COLL_REDUCESCATTER = 3 };
-enum { POLAR_ALGO_TREE = 0, POLAR_ALGO_RING = 1, POLAR_ALGO_NVLS = 2 /* reserved */,
+enum { POLAR_ALGO_TREE = 0, POLAR_ALGO_RING = 1, POLAR_ALGO_NVLS = 2 /* switch reduction, f1 */,
        POLAR_ALGO_ONESHOT = 3, POLAR_ALGO_TWOSHOT = 4 };
 enum { POLAR_PROTO_LL = 0, POLAR_PROTO_LL128 = 1, POLAR_PROTO_SIMPLE = 2 };
 
@@ -320,6 +320,28 @@ polar_status polar_all_gather_v(polar_comm_t comm, void* const* sendbufs, void* 
 polar_status polar_broadcast(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, int root, void* stream);
 polar_status polar_broadcast_v(polar_comm_t comm, void* const* bufs, size_t count, polar_dtype dtype, int root,
                                void* stream);
+
+/* ----------------------------------------------------------- NVLS
+ * POLAR_ALGO_NVLS reduces inside the NVSwitch (NCCL's
+ * default, 836.3 GB/s at 8 GiB on the paper's node): polar_comm_init creates one
+ * multicast object over the comm's GPUs (cuMulticastCreate; FABRIC handle, else
+ * a POSIX fd copied with pidfd_getfd), binds POLAR_NVLS_BYTES (default 256 MiB,
+ * POLAR_NVLS=0 disables) of every rank's memory to it, and an NVLS AllReduce
+ * copies the message into that region, runs `multimem.ld_reduce` + `multimem.st`
+ * over each rank's shard between an entry and an exit barrier, and copies the
+ * result out (chunked by the region).  The switch's f32 summation order is
+ * unspecified: results are within R2's bound, not bit-equal to the rank-order
+ * oracle; bf16 accumulates in f32 and rounds once; integers are exact; f32
+ * min / max do not exist in the switch (POLAR_EUNSUPPORTED).  Comms without a
+ * multicast object (virtual comms; nodes whose driver refuses multicast) return
+ * POLAR_EUNSUPPORTED for NVLS decisions.
+ * polar_nvls_available: 1 while some comm of this process holds a multicast
+ * object (polar_set_policy accepts NVLS rows only then).
+ * polar_comm_nvls_info: *available = 1 if this comm holds one; `why` (may be
+ * NULL) receives the object's description or the first failing driver call,
+ * its CUresult name and the rank it failed on. */
+int polar_nvls_available(void);
+polar_status polar_comm_nvls_info(polar_comm_t comm, int* available, char* why, size_t len);
 
 /* Decision used by the most recent AllReduce on this comm. */
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);

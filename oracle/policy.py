@@ -97,7 +97,7 @@ def decide(rows, coll: int, nranks: int, nbytes: int):
     return None if r is None else r[:3]
 
 
-def validate(rows) -> str:
+def validate(rows, nvls_available: bool = False) -> str:
     """Status name set_policy must return for ``rows``.
 
     "ok", or "einval" (malformed: too many rows, unknown enum, nranks > 8,
@@ -132,7 +132,7 @@ def validate(rows) -> str:
         if key in last and max_bytes <= last[key]:
             return "einval"
         last[key] = max_bytes
-        if algo == NVLS:
+        if algo == NVLS and (not nvls_available or coll != COLL_ALLREDUCE):
             unsupported = True
         if coll != COLL_ALLREDUCE and (algo not in (ONESHOT, UNSET) or proto not in (SIMPLE, UNSET)):
             unsupported = True

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -78,6 +79,12 @@ Layout make_layout(bool with_bounce) {
     L.bounce_bytes = with_bounce ? align_up(env_size("POLAR_BOUNCE", 64 << 20), 4096) : 0;
     L.bounce_off = off; off = align_up(off + L.bounce_bytes, 4096);
     L.total = off;
+    // NVLS: the region bound to the multicast object (real comms; every rank the same)
+    L.nvls_bytes = with_bounce ? align_up(env_size("POLAR_NVLS_BYTES", 256 << 20), 2 << 20) : 0;
+    {
+        const char* e = std::getenv("POLAR_NVLS");
+        if (e && e[0] == '0') L.nvls_bytes = 0;
+    }
     return L;
 }
 
@@ -131,11 +138,15 @@ struct polar_comm_s {
     unsigned long long tel_seq = 0;      // last launch sequence number handed out
     unsigned long long tel_consumed = 0; // samples consumed up to (and including) this seq
     int tma_mode = 2;                    // two-shot Simple via TMA smem staging: 0 never, 1 always, 2 auto
+    int ring_tma = 0;                    // ring Simple via TMA-staged FIFOs (POLAR_RING_TMA=1 enables)
+    size_t ring_tma_min = 0;             // ... from this many bytes per channel on (POLAR_RING_TMA_MIN)
+    int ring_flags = 1;                  // ring_simple_tma: bit 0 L2 hints, bit 1 discard (POLAR_RING_TMA_FLAGS)
     unsigned long long timeout_ns = 0;
     // polar_allreduce_host chunk pipeline (created on first use)
     cudaStream_t hs_in = nullptr, hs_out = nullptr;
     cudaEvent_t he_start = nullptr, he_in = nullptr, he_red = nullptr, he_out = nullptr;
     unsigned long long probe_epoch = 0;  // p2p probe calls (same count on every rank)
+    NvlsState nvls;                      // switch reduction (f1): multicast object, if the node has one
     std::mutex mu;
 };
 
@@ -212,6 +223,7 @@ polar_status check_latched(polar_comm_s* c) {
 // and offset, bounce, staged), so that ranks which took different paths for one
 // call disagree in the tag.
 constexpr uint64_t kPathBounce = 0xB0B0ull;   // two-shot through the scratch bounce region
+constexpr uint64_t kPathNvls = 0x4E564Cull;    // NVLS through the multicast-bound region
 
 uint64_t decision_tag(int kind, int algo, int proto, int nch, int dtype, int op, uint64_t count, int root,
                       uint64_t path = 0) {
@@ -296,15 +308,30 @@ polar_status alloc_common(polar_comm_s* c) {
         c->jitter_ns = (unsigned)env_size("POLAR_JITTER_NS", 0);
         const char* et = std::getenv("POLAR_TWOSHOT_TMA");
         c->tma_mode = et ? (et[0] == '1' ? 1 : 0) : 2;
+        // TMA-staged ring Simple: opt-in (POLAR_RING_TMA=1).  On one GPU it is not
+        // faster than the warp-specialised LDG ring (both sit at the memory-op
+        // throughput of one HBM, DESIGN.md §8 "Ring on virtual ranks"), and bulk
+        // copies over peer-mapped NVLink memory are not validated on this pool.
+        const char* er = std::getenv("POLAR_RING_TMA");
+        c->ring_tma = er && er[0] == '1';
+        c->ring_tma_min = env_size("POLAR_RING_TMA_MIN", 0);
+        {
+            const char* ef = std::getenv("POLAR_RING_TMA_FLAGS");
+            if (ef && *ef) c->ring_flags = (int)std::strtol(ef, nullptr, 0);
+        }
     }
     // the two-shot Simple kernels may use up to tma_smem_bytes(8) of dynamic shared memory
     const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
     const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
     for (int dt : dts)
-        for (int op : ops)
+        for (int op : ops) {
             CU_TRY(cudaFuncSetAttribute(kernel_for(dt, op, POLAR_ALGO_TWOSHOT, POLAR_PROTO_SIMPLE),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)dev::tma_smem_bytes(kMaxRanks)));
+            CU_TRY(cudaFuncSetAttribute(kernel_for(dt, op, POLAR_ALGO_RING, POLAR_PROTO_SIMPLE),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dev::ring_tma_smem_bytes()));
+        }
     c->timeout_ns = (unsigned long long)env_size("POLAR_TIMEOUT_MS", 20000) * 1000000ull;
     CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
     *c->err_host = 0;
@@ -402,6 +429,7 @@ void destroy_comm(polar_comm_s* c, bool collective) {
     DeviceGuard dg(c->device);
     cudaDeviceSynchronize();
     if (collective) (void)host_barrier(c);
+    nvls_teardown(c->nvls, c->device);
     for (char* m : c->ipc_mapped) cudaIpcCloseMemHandle(m);
     for (auto& r : c->regs)
         if (r.owned) cudaFree(r.base);
@@ -559,7 +587,9 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         st = polar_decide(&ctx, &d);
         if (st != POLAR_OK) return st;
     }
-    const void* fn = kernel_for(dtype, op, (int)d.algo, (int)d.proto);
+    const bool nvls = d.algo == POLAR_ALGO_NVLS;
+    const void* fn = nvls ? (c->nvls.ok ? nvls_kernel_for(dtype, op) : nullptr)
+                          : kernel_for(dtype, op, (int)d.algo, (int)d.proto);
     if (!fn) return POLAR_EUNSUPPORTED;
     c->last = d;                      // the policy's decision (what the hook returned)
     const bool adaptive_row = (d.flags & POLAR_ROW_ADAPTIVE_NCH) && count > 0 && c->nranks > 1;
@@ -601,7 +631,10 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     const bool ts_simple = d.algo == POLAR_ALGO_TWOSHOT && d.proto == POLAR_PROTO_SIMPLE;
     const bool tma_auto = c->is_virtual && c->nranks <= 4 && count * (size_t)es >= (64u << 20);
     P.tma = (ts_simple && (c->tma_mode == 1 || (c->tma_mode == 2 && tma_auto))) ? 1 : 0;
-    const size_t smem = P.tma ? dev::tma_smem_bytes(c->nranks) : 0;
+    const bool ring_simple = d.algo == POLAR_ALGO_RING && d.proto == POLAR_PROTO_SIMPLE;
+    P.ring_tma = (ring_simple && c->ring_tma && count * (size_t)es / d.nchannels >= c->ring_tma_min) ? 1 : 0;
+    P.ring_flags = c->ring_flags;
+    const size_t smem = P.tma ? dev::tma_smem_bytes(c->nranks) : (P.ring_tma ? dev::ring_tma_smem_bytes() : 0);
     const size_t bytes = count * (size_t)es;
 
     if (c->is_virtual) {
@@ -615,6 +648,26 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
     char* mine = reinterpret_cast<char*>(bufs[0]);
+    if (nvls) {
+        // switch reduction over the bound region (nvls.cu): every rank copies its
+        // input in, the kernel reduces through the multicast mapping, every rank
+        // copies the result out; chunked by the region (minus one pad pack)
+        const size_t chunk_elems = std::max<size_t>(16 / es, ((c->nvls.bytes - 16) / es) / (16 / es) * (16 / es));
+        P.bufs[c->rank0] = c->nvls.uc;
+        P.recv[0] = c->nvls.mc;
+        P.vec = 1;
+        for (size_t done = 0; done < count; done += chunk_elems) {
+            const size_t n = std::min(chunk_elems, count - done);
+            char* src = mine + done * es;
+            CU_TRY(cudaMemcpyAsync(c->nvls.uc, src, n * es, cudaMemcpyDeviceToDevice, stream));
+            P.count = n;
+            P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, n, 0, kPathNvls);
+            st = launch_kernel(c, fn, P, grid, stream, 0);
+            if (st != POLAR_OK) return st;
+            CU_TRY(cudaMemcpyAsync(src, c->nvls.uc, n * es, cudaMemcpyDeviceToDevice, stream));
+        }
+        return POLAR_OK;
+    }
     if (d.algo != POLAR_ALGO_TWOSHOT || d.proto != POLAR_PROTO_SIMPLE) {
         // only the local buffer is touched directly; peers go through scratch
         P.bufs[c->rank0] = mine;
@@ -773,6 +826,10 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     // safe: a rank's own current kernel is always fully resident first.
     if (shared_gpu) c->pdl = false;
     if (st == POLAR_OK) st = exchange_and_map(c, c->scratch_own[0], c->scratch);
+    if (st == POLAR_OK && nranks > 1 && c->L.nvls_bytes)
+        st = nvls_setup(c->nvls, nranks, rank, cuda_device, ag, user, c->L.nvls_bytes);
+    else if (st == POLAR_OK)
+        std::snprintf(c->nvls.why, sizeof(c->nvls.why), "%s", nranks > 1 ? "disabled (POLAR_NVLS=0)" : "one rank");
     if (st == POLAR_OK) st = init_barrier(c);
     if (st != POLAR_OK) { destroy_comm(c, false); return st; }
     *out = c;
@@ -806,6 +863,8 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
         c->coop = ev && ev[0] == '1';
     }
     c->L = make_layout(false);
+    std::snprintf(c->nvls.why, sizeof(c->nvls.why),
+                  "virtual comm: every rank on one device (a multicast object binds one region per device)");
     DeviceGuard dg(cuda_device);
     polar_status st = dg.ok ? POLAR_OK : POLAR_ECUDA;
     if (st == POLAR_OK) st = alloc_common(c);
@@ -1053,6 +1112,13 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
     CU_TRY(cudaStreamWaitEvent(s, comm->he_out, 0));
     CU_TRY(cudaStreamSynchronize(s));
     return check_latched(comm);
+}
+
+polar_status polar_comm_nvls_info(polar_comm_t comm, int* available, char* why, size_t len) {
+    if (!comm) return POLAR_EINVAL;
+    if (available) *available = comm->nvls.ok ? 1 : 0;
+    if (why && len) std::snprintf(why, len, "%s", comm->nvls.why);
+    return POLAR_OK;
 }
 
 polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out) {

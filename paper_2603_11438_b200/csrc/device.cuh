@@ -43,6 +43,8 @@ struct Params {
     unsigned long long* trace;  // optional per-CTA timestamps (polar_comm_set_trace), else null
     int sys;                    // 1: peers are other GPUs (system-scope ordering); 0: one GPU (gpu scope)
     int tma;                    // two-shot Simple: 1 = TMA bulk-copy staging through shared memory
+    int ring_tma;               // ring Simple: 1 = TMA-staged FIFO kernel (ring_simple_tma) where eligible
+    int ring_flags;             // ring_simple_tma: bit 0 = L2 eviction hints, bit 1 = discard consumed FIFO lines
     unsigned jitter_ns;         // fault injection: random __nanosleep (< jitter_ns) before 1/8 of all
                                 // signal and LL stores (POLAR_JITTER_NS; 0 = off)
     TelEntry* tel;              // profiler telemetry ring (host-mapped), or null
@@ -188,6 +190,22 @@ __host__ __device__ constexpr size_t tma_smem_bytes(int /*n*/) {
     return (size_t)kTmaStages * kTmaStageBytes + kTmaStages * (8 + 8 + 8 + 8) + 128;
 }
 
+// TMA-staged ring Simple (kernels.cuh ring_simple_tma): stages of one tile =
+// the predecessor's FIFO words (sized for bf16's 2 f32 words per pack) + my packs
+#ifndef POLAR_RING_TMA_STAGES
+#define POLAR_RING_TMA_STAGES 6
+#endif
+#ifndef POLAR_RING_TMA_TILE
+#define POLAR_RING_TMA_TILE 512
+#endif
+constexpr int kRtStages = POLAR_RING_TMA_STAGES;
+constexpr unsigned kRtTile = POLAR_RING_TMA_TILE;       // element packs per tile (8 KiB of elements)
+constexpr size_t kRtInBytes = (size_t)kRtTile * 16 * 2; // FIFO words of a tile, sized for AW = 2
+constexpr size_t kRtStageBytes = kRtInBytes + (size_t)kRtTile * 16;
+__host__ __device__ constexpr size_t ring_tma_smem_bytes() {
+    return (size_t)kRtStages * kRtStageBytes + (size_t)kRtStages * 3 * 8 + 64;
+}
+
 // cp.async.bulk (SASS UBLKCP) moves whole tiles between global memory (local or
 // peer-mapped) and shared memory; completion of loads is tracked by an mbarrier
 // transaction count, stores by bulk async-groups.
@@ -225,9 +243,38 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                  "r"(bytes)
                  : "memory");
 }
+// L2 eviction-priority policies for bulk copies (createpolicy; SASS UBLKCP with a
+// cache-policy operand): streaming data evict_first, FIFO lines that the
+// consumer reads soon evict_last.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                               uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* smem_src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait_group() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

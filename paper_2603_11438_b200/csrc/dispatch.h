@@ -17,6 +17,10 @@ const void* direct_kernel_i64(int mode, int op);
 const void* direct_kernel_f32(int mode, int op);
 const void* direct_kernel_bf16(int mode, int op);
 
+// NVLS (switch reduction, nvls.cu): nullptr where the switch has no such
+// reduction (f32 min / max)
+const void* nvls_kernel_for(int dtype, int op);
+
 inline const void* direct_kernel_for(int dtype, int mode, int op) {
     switch (dtype) {
         case POLAR_INT32: return direct_kernel_i32(mode, op);

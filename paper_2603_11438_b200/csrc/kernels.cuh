@@ -1299,6 +1299,337 @@ __device__ void ring_simple_ws(const Params& P, const Who& w) {
     }
 }
 
+
+// Ring Simple, TMA-staged (POLAR_RING_TMA).  The warp-specialised
+// ring above is limited by loads in flight per data thread (ncu: 40 % long-
+// scoreboard stalls, L2 36 % / DRAM 53 % of peak) and the register cap.  Here
+// the FIFO and own-buffer traffic moves as cp.async.bulk copies through
+// shared-memory stages, so bytes in flight cost no registers:
+//   warp 0  sync     : unchanged role (polls fills / credits, hands a unit over
+//                      with READY, publishes unit g-1 after DONE(g-1))
+//   warp 1  loader   : after READY(g), per tile of unit g: one bulk load of the
+//                      predecessor's FIFO words and one of my own packs into a
+//                      stage (`full` mbarrier counts the bytes)
+//   warp 2  storer   : per tile, once the consumers are done (`cons`): bulk
+//                      stores of the result to the successor's FIFO and/or my
+//                      buffer; frees a stage once its stores have read it
+//                      (`empty`, lagged by one tile); at a unit's end waits for
+//                      its writes (wait_group 0 + proxy fence) and arrives DONE(g)
+//   warps 3+ consumers: reduce in shared memory (reduce-scatter steps only)
+// Tile kinds per step s (AW = accumulator words: 2 for bf16's f32 partials):
+//   s = 0        own -> [widen] -> next FIFO (AW words)
+//   0 < s < n-1  FIFO (AW) (op) own -> next FIFO (AW)
+//   s = n-1      fin(FIFO (AW) (op) own) -> own buffer + next FIFO (1 word)
+//   s >= n       FIFO (1) -> own buffer (+ next FIFO unless last)  (no compute)
+// Same units, tails, credits and slot layout as ring_simple_ws, so the two
+// kernels share FIFOs and counters across calls; used when every pack is a
+// full 16-B pack of a 16-B aligned buffer (bulk copies are 16-B granular),
+// else ring_simple_ws runs.
+#ifndef POLAR_RING_TMA
+#define POLAR_RING_TMA 1
+#endif
+// (stage geometry: device.cuh kRtStages / kRtTile / ring_tma_smem_bytes)
+
+// Walk the ring schedule of one channel exactly as ring_simple_ws does: for each
+// unit (sub-slice q of step s of a lap) call unit(g, s, q, ...), and for each
+// tile of it tile(t, s, i0, npk, j0, src, dst).  Every role of the kernel walks
+// the same sequence, so tile t and unit g mean the same thing to all of them.
+template <int DT, class FU, class FT>
+__device__ __forceinline__ bool ring_tma_walk(const Params& P, int r, int n, int c, unsigned long long ca,
+                                              unsigned long long cb, unsigned long long SP, unsigned long long sent,
+                                              unsigned long long recvd, FU&& unit, FT&& tile) {
+    constexpr int RQ = POLAR_RING_WS_SUB;
+    const int next = (r + 1) % n;
+    const unsigned long long LC = SP * (unsigned long long)n;
+    unsigned long long g = 0, t = 0;
+    for (unsigned long long base = ca; base < cb; base += LC) {
+        const unsigned long long L = (cb - base < LC) ? cb - base : LC;
+        for (int s = 0; s < 2 * (n - 1) + 1; ++s) {
+            int k;
+            if (s < n) k = ((r - s) % n + n) % n;
+            else k = ((r - (s - n)) % n + n) % n;
+            if (s == n - 1) k = (r + 1) % n;
+            const unsigned long long ks = base + L * (unsigned long long)k / n;
+            const unsigned long long ke = base + L * (unsigned long long)(k + 1) / n;
+            const uint4* src = ring_slot<POLAR_PROTO_SIMPLE>(P, r, c, recvd);
+            uint4* dst = ring_slot<POLAR_PROTO_SIMPLE>(P, next, c, sent);
+            for (int q = 0; q < RQ; ++q) {
+                const unsigned long long qs = ks + (ke - ks) * (unsigned long long)q / RQ;
+                const unsigned long long qe = ks + (ke - ks) * (unsigned long long)(q + 1) / RQ;
+                if (!unit(g, s, q, true)) return false;
+                for (unsigned long long i0 = qs; i0 < qe; i0 += kRtTile) {
+                    const unsigned npk = (unsigned)((qe - i0) < kRtTile ? (qe - i0) : kRtTile);
+                    if (!tile(t, s, i0, npk, i0 - ks, src, dst)) return false;
+                    ++t;
+                }
+                if (!unit(g, s, q, false)) return false;
+                ++g;
+            }
+            if (s < 2 * (n - 1)) ++sent;
+            if (s > 0) ++recvd;
+        }
+    }
+    return true;
+}
+
+template <int DT, int OP>
+__device__ void ring_simple_tma(const Params& P, const Who& w) {
+    constexpr int AW = AccWords<DT>::N;
+    constexpr int RQ = POLAR_RING_WS_SUB;
+    static_assert(RQ >= 2, "the publication lag needs >= 2 sub-slices per slot");
+    constexpr int kReady = 1, kDone = 3;
+    const int n = w.n, tid = w.tid, r = w.r, c = w.c;
+    const int next = (r + 1) % n, prev = (r + n - 1) % n;
+    const int warp = tid >> 5, lane = tid & 31;
+    ChanState* st = chan_state(P, r, c);
+    const unsigned long long sent0 = st->ring_sent, recvd0 = st->ring_recv;
+    const unsigned long long SP = Wire<POLAR_PROTO_SIMPLE>::units(P.ring_slot) / AW;   // element packs per slot
+    unsigned long long ca, cb;
+    split_range(0, npacks<DType<DT>::ES>(P), P.nch, c, ca, cb);
+    char* mine = P.bufs[r];
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kRtStages * kRtStageBytes);
+    uint64_t* cons = full + kRtStages;
+    uint64_t* empty = cons + kRtStages;
+    const int ncons_warps = (int)(blockDim.x >> 5) - 3;
+    __shared__ int s_abort;
+    if (tid == 0) {
+        s_abort = 0;
+        for (int x = 0; x < kRtStages; ++x) {
+            mbar_init(&full[x], 1);
+            mbar_init(&cons[x], (uint32_t)ncons_warps);
+            mbar_init(&empty[x], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto in_smem = [&](unsigned long long t) { return smem + (size_t)(t % kRtStages) * kRtStageBytes; };
+    auto own_smem = [&](unsigned long long t) { return smem + (size_t)(t % kRtStages) * kRtStageBytes + kRtInBytes; };
+    auto in_words = [&](int s) { return s == 0 ? 0 : (s <= n - 1 ? AW : 1); };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ sync warp
+        uint64_t* head_in = flag_ptr(P, r, F_RING_HEAD, c, 0);
+        uint64_t* tail_in = flag_ptr(P, r, F_RING_TAIL, c, 0);
+        uint64_t* tail_out = flag_ptr(P, next, F_RING_TAIL, c, 0);
+        uint64_t* head_out = flag_ptr(P, prev, F_RING_HEAD, c, 0);
+        unsigned long long sent = sent0, recvd = recvd0, gpub = 0;
+        uint64_t seen = 0, pub_tail = 0, pub_head = 0;
+        auto publish = [&]() {
+            nbar_sync(kDone + (int)((gpub - 1) & 1), 64);   // unit g-1's writes are complete (storer)
+            if (lane == 0) {
+                fence_acq_rel(P.sys);
+                if (pub_tail) jitter(P), st_relaxed(tail_out, pub_tail, P.sys);
+                if (pub_head) jitter(P), st_relaxed(head_out, pub_head, P.sys);
+            }
+        };
+        const bool ok = ring_tma_walk<DT>(P, r, n, c, ca, cb, SP, sent0, recvd0,
+            [&](unsigned long long g, int s, int q, bool begin) {
+                if (!begin) {
+                    if (q == RQ - 1) {
+                        if (s < 2 * (n - 1)) ++sent;
+                        if (s > 0) ++recvd;
+                    }
+                    return true;
+                }
+                const bool do_recv = s > 0, do_send = s < 2 * (n - 1);
+                int okw = 1;
+                if (lane == 0 && do_recv) okw = wait_cached(P, tail_in, recvd * RQ + q + 1, seen);
+                if (lane == 1 && q == 0 && do_send && sent >= (unsigned long long)kSteps)
+                    okw = wait_cached(P, head_in, sent - kSteps + 1, seen);
+                okw = __all_sync(0xffffffffu, okw);
+                if (!okw && lane == 0) *(volatile int*)&s_abort = 1;
+                __syncwarp();
+                nbar_arrive(kReady + (int)(g & 1), 64);
+                if (!okw) return false;
+                if (g > 0) publish();
+                pub_tail = do_send ? sent * RQ + q + 1 : 0;
+                pub_head = (do_recv && q == RQ - 1) ? recvd + 1 : 0;
+                gpub = g + 1;
+                return true;
+            },
+            [&](unsigned long long, int, unsigned long long, unsigned, unsigned long long, const uint4*, uint4*) {
+                return true;
+            });
+        if (!ok) return;
+        if (gpub > 0) publish();
+        if (lane == 0) {
+            st->ring_sent = sent;
+            st->ring_recv = recvd;
+        }
+        return;
+    }
+    if (warp == 1) {
+        // -------------------------------------------------------------- loader
+        unsigned long long issued = 0;   // tiles issued so far
+        const uint64_t pol_first = l2_evict_first();
+        const bool ok = ring_tma_walk<DT>(P, r, n, c, ca, cb, SP, sent0, recvd0,
+            [&](unsigned long long g, int, int, bool begin) {
+                if (!begin) return true;
+                nbar_sync(kReady + (int)(g & 1), 64);
+                if (*(volatile int*)&s_abort) return false;
+                if (lane == 0) fence_proxy_async_global();   // the fills acquired by the sync warp -> bulk reads
+                return true;
+            },
+            [&](unsigned long long t, int s, unsigned long long i0, unsigned npk, unsigned long long j0,
+                const uint4* src, uint4*) {
+                int ab = 0;
+                if (lane == 0) {
+                    const int x = (int)(t % kRtStages);
+                    if (t >= (unsigned long long)kRtStages)
+                        while (!mbar_try_wait(&empty[x], (uint32_t)((t / kRtStages - 1) & 1)))
+                            if (*(volatile int*)&s_abort) { ab = 1; break; }
+                }
+                if (__shfl_sync(0xffffffffu, ab, 0)) return false;
+                if (lane == 0) {
+                    const int x = (int)(t % kRtStages);
+                    const int wi = in_words(s);
+                    const bool own = s <= n - 1;
+                    const uint32_t bin = npk * 16u * (uint32_t)wi, bown = own ? npk * 16u : 0u;
+                    mbar_arrive_expect_tx(&full[x], bin + bown);
+                    const char* fsrc = reinterpret_cast<const char*>(src) + j0 * 16ull * wi;
+                    if (P.ring_flags & 1) {
+                        // both are read once here: evict first
+                        if (bin) bulk_load_hint(in_smem(t), fsrc, bin, &full[x], pol_first);
+                        if (bown) bulk_load_hint(own_smem(t), mine + i0 * 16ull, bown, &full[x], pol_first);
+                    } else {
+                        if (bin) bulk_load(in_smem(t), fsrc, bin, &full[x]);
+                        if (bown) bulk_load(own_smem(t), mine + i0 * 16ull, bown, &full[x]);
+                    }
+                }
+                issued = t + 1;
+                return true;
+            });
+        if (!ok && lane == 0) {
+            // aborted (a peer timed out): every bulk load issued must land before
+            // this CTA's shared memory goes away; no newer phase is ever started
+            const unsigned long long lo = issued > (unsigned long long)kRtStages ? issued - kRtStages : 0;
+            for (unsigned long long t = lo; t < issued; ++t)
+                while (!mbar_try_wait(&full[t % kRtStages], (uint32_t)((t / kRtStages) & 1))) {}
+        }
+        return;
+    }
+    if (warp == 2) {
+        // -------------------------------------------------------------- storer
+        long long pending = -1;   // tile whose stage is released once its stores have read it
+        const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
+        // DONE(g) once unit g's writes are complete.  (Arriving it lazily, after
+        // the next unit's first tile with wait_group 1, was measured slower: the
+        // later publication lengthens every hop of the ring's chain — 8 MiB
+        // 85 -> 106 us, 128 MiB 1079 -> 1128 us; profiles/r02_ring_tma_ab.jsonl.)
+        ring_tma_walk<DT>(P, r, n, c, ca, cb, SP, sent0, recvd0,
+            [&](unsigned long long g, int, int, bool begin) {
+                if (begin) return true;
+                if (lane == 0) {
+                    bulk_wait_all();                   // unit g's writes are complete
+                    if (pending >= 0) mbar_arrive(&empty[pending % kRtStages]);
+                    fence_proxy_async_global();        // async-proxy writes -> the sync warp's fence + flag
+                }
+                pending = -1;
+                __syncwarp();
+                nbar_arrive(kDone + (int)(g & 1), 64);
+                return true;
+            },
+            [&](unsigned long long t, int s, unsigned long long i0, unsigned npk, unsigned long long j0,
+                const uint4* src, uint4* dst) {
+                const int x = (int)(t % kRtStages);
+                int ab = 0;
+                if (lane == 0) {
+                    while (!mbar_try_wait(&cons[x], (uint32_t)((t / kRtStages) & 1)))
+                        if (*(volatile int*)&s_abort) break;
+                    ab = *(volatile int*)&s_abort;
+                }
+                ab = __shfl_sync(0xffffffffu, ab, 0);
+                if (!ab && (P.ring_flags & 2) && s > 0) {
+                    // The tile's FIFO words are in shared memory now (cons implies the
+                    // loads landed) and the slot is rewritten by the predecessor only
+                    // after our credit: drop its lines from L2 without write-back
+                    // (whole 128-B lines inside the tile only: a boundary line may
+                    // hold words of a neighbour tile not loaded yet).
+                    const int wi = in_words(s);
+                    const unsigned long long a = reinterpret_cast<unsigned long long>(src) + j0 * 16ull * wi;
+                    const unsigned long long e = a + (unsigned long long)npk * 16ull * wi;
+                    for (unsigned long long l = ((a + 127) & ~127ull) + (unsigned long long)lane * 128; l + 128 <= e;
+                         l += 32 * 128)
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    if (!ab) {
+                        const bool first = s == 0, fin = s == n - 1, ag = s >= n;
+                        const bool send = s < 2 * (n - 1);
+                        // which stage region holds the result, and how many words per pack
+                        const void* res;
+                        int wo;
+                        if (fin) { res = own_smem(t); wo = 1; }
+                        else if (ag) { res = in_smem(t); wo = 1; }
+                        else if (first && AW == 1) { res = own_smem(t); wo = 1; }
+                        else { res = in_smem(t); wo = AW; }
+                        char* fdst = reinterpret_cast<char*>(dst) + j0 * 16ull * wo;
+                        if (P.ring_flags & 1) {
+                            // FIFO words are read soon by the successor: keep them; my result is streaming
+                            if (send) bulk_store_hint(fdst, res, npk * 16u * (uint32_t)wo, pol_last);
+                            if (fin || ag) bulk_store_hint(mine + i0 * 16ull, res, npk * 16u, pol_first);
+                        } else {
+                            if (send) bulk_store(fdst, res, npk * 16u * (uint32_t)wo);
+                            if (fin || ag) bulk_store(mine + i0 * 16ull, res, npk * 16u);
+                        }
+                        bulk_commit();
+                        bulk_wait_read<1>();               // the previous tile's stores have read its stage
+                        if (pending >= 0) mbar_arrive(&empty[pending % kRtStages]);
+                    }
+                }
+                if (ab) {
+                    if (lane == 0) bulk_wait_all();   // no store may still read this CTA's shared memory
+                    return false;
+                }
+                pending = (long long)t;
+                return true;
+            });
+        return;
+    }
+    // ------------------------------------------------------------------ consumers
+    const unsigned ct = (unsigned)(tid - 96), nct = blockDim.x - 96;
+    ring_tma_walk<DT>(P, r, n, c, ca, cb, SP, sent0, recvd0,
+        [&](unsigned long long, int, int, bool) { return true; },
+        [&](unsigned long long t, int s, unsigned long long, unsigned npk, unsigned long long, const uint4*, uint4*) {
+            const int x = (int)(t % kRtStages);
+            while (!mbar_try_wait(&full[x], (uint32_t)((t / kRtStages) & 1)))
+                if (*(volatile int*)&s_abort) break;
+            const bool ab = *(volatile int*)&s_abort != 0;
+            if (!ab) {
+                uint4* in = reinterpret_cast<uint4*>(in_smem(t));
+                uint4* own = reinterpret_cast<uint4*>(own_smem(t));
+                if (s == 0) {
+                    if (AW > 1)
+                        for (unsigned j = ct; j < npk; j += nct) {
+                            Acc<DT> acc;
+                            acc_init<DT>(acc, own[j]);
+#pragma unroll
+                            for (int y = 0; y < AW; ++y) in[j * AW + y] = acc.w[y];
+                        }
+                } else if (s < n) {
+                    for (unsigned j = ct; j < npk; j += nct) {
+                        Acc<DT> acc;
+#pragma unroll
+                        for (int y = 0; y < AW; ++y) acc.w[y] = in[j * AW + y];
+                        acc_add<DT, OP>(acc, own[j]);
+                        if (s < n - 1) {
+#pragma unroll
+                            for (int y = 0; y < AW; ++y) in[j * AW + y] = acc.w[y];
+                        } else {
+                            own[j] = acc_fin<DT>(acc);
+                        }
+                    }
+                }
+                if (s < n) fence_proxy_async_smem();   // my smem writes -> the bulk stores
+            }
+            __syncwarp();
+            if (!ab && lane == 0) mbar_arrive(&cons[x]);
+            return !ab;
+        });
+}
+
 // ======================================================================= tree
 // Binary tree per channel over positions pos = (rank - c) mod n (root = rank c
 // mod n); children 2pos+1, 2pos+2.  Up phase: node = own (op) child0 (op)
@@ -1790,8 +2121,15 @@ __global__ void __launch_bounds__(kBlock, POLAR_LB_MIN) allreduce_kernel(Params 
         if constexpr (PROTO == POLAR_PROTO_SIMPLE) oneshot_simple<DT, OP>(P, w);
         else oneshot_ll<DT, OP, PROTO>(P, w);
     } else if constexpr (ALGO == POLAR_ALGO_RING) {
-        if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_RING_WS) ring_simple_ws<DT, OP>(P, w);
-        else ring<DT, OP, PROTO>(P, w);
+        if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_RING_WS) {
+            // TMA staging needs whole 16-B packs of a 16-B aligned buffer (uniform per launch)
+            if (POLAR_RING_TMA && P.ring_tma && P.vec && (P.count * DType<DT>::ES) % 16 == 0)
+                ring_simple_tma<DT, OP>(P, w);
+            else
+                ring_simple_ws<DT, OP>(P, w);
+        } else {
+            ring<DT, OP, PROTO>(P, w);
+        }
     } else {
         if constexpr (PROTO == POLAR_PROTO_SIMPLE && POLAR_TREE_WS) tree_simple_ws<DT, OP>(P, w);
         else tree<DT, OP, PROTO>(P, w);

@@ -70,6 +70,7 @@ struct Layout {
     size_t tree128_off, tree128_slot; // tree LL128: up [kMaxCh][2][kSteps], down [kMaxCh][kSteps]
     size_t bounce_off, bounce_bytes;  // two-shot bounce for unregistered buffers (real comms)
     size_t total;
+    size_t nvls_bytes;                // NVLS region per rank (POLAR_NVLS_BYTES; 0 = NVLS off), not in scratch
 };
 #ifndef POLAR_FIFO_STEPS
 #define POLAR_FIFO_STEPS 4
@@ -77,6 +78,28 @@ struct Layout {
 constexpr int kSteps = POLAR_FIFO_STEPS;  // FIFO depth (slots) per connection
 
 Layout make_layout(bool with_bounce);
+
+// ------------------------------------------------------- NVLS (f1, nvls_host.cpp)
+struct NvlsState {
+    bool ok = false;                    // a multicast object is bound on every rank
+    bool bound = false;
+    int status = 0;                     // CUresult of the first failure (0 = none)
+    int handle_type = 0;                // CUmemAllocationHandleType used to share the object
+    int fd = -1;                        // rank 0, POSIX handle: kept open for the comm's life
+    size_t bytes = 0;                   // bound region per rank
+    unsigned long long mc_handle = 0;   // CUmemGenericAllocationHandle of the multicast object
+    unsigned long long phys = 0;        // this rank's bound physical allocation
+    char* uc = nullptr;                 // this rank's bound copy (unicast mapping)
+    char* mc = nullptr;                 // the multicast mapping of the same region
+    char why[192] = {};                 // what happened (the first failing call, or the object)
+};
+// Collective over the bootstrap all-gather (same number of all-gathers on every
+// rank whatever fails).  POLAR_OK with s.ok == false when NVLS is unavailable
+// (s.why says why); POLAR_ESTATE only if the all-gather itself failed.
+polar_status nvls_setup(NvlsState& s, int nranks, int rank, int device, polar_allgather_fn ag, void* user,
+                        size_t bytes);
+void nvls_teardown(NvlsState& s, int device);
+bool nvls_available();   // some comm of this process holds a multicast object
 
 // ---------------------------------------------------- adaptive channels (f3)
 struct Adaptive {

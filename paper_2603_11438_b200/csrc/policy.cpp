@@ -67,7 +67,11 @@ polar_status validate_rows(const polar_policy_row* rows, uint32_t nrows) {
         switch (r.algo) {
             case POLAR_ALGO_TREE: case POLAR_ALGO_RING: case POLAR_ALGO_ONESHOT:
             case POLAR_ALGO_TWOSHOT: case POLAR_UNSET: break;
-            case POLAR_ALGO_NVLS: unsupported = true; break;
+            case POLAR_ALGO_NVLS:
+                // accepted only while some comm holds a multicast object (nvls_host.cpp);
+                // ReduceScatter / AllGather / Broadcast have no NVLS kernel
+                if (!polar::nvls_available() || r.coll != POLAR_COLL_ALLREDUCE) unsupported = true;
+                break;
             default: return POLAR_EINVAL;
         }
         switch (r.proto) {

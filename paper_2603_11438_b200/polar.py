@@ -136,6 +136,8 @@ _sigs = {
     "polar_adaptive_inject": (C.c_int, [_P, C.c_double]),
     "polar_adaptive_simulate": (C.c_int, [C.POINTER(AdaptiveParams), C.c_uint32, C.POINTER(C.c_double), C.c_uint32,
                                           C.POINTER(C.c_uint32)]),
+    "polar_nvls_available": (C.c_int, []),
+    "polar_comm_nvls_info": (C.c_int, [_P, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     "polar_status_string": (C.c_char_p, [C.c_int]),
     "polar_version": (C.c_char_p, []),
 
@@ -486,6 +488,14 @@ class Comm:
 
     def check(self):
         _check(lib.polar_comm_check(self.h), "polar_comm_check")
+
+    def nvls_info(self):
+        """(available, why): does this comm hold a multicast object (NVLS), and
+        the object's description or the driver call that refused it."""
+        av = C.c_int(0)
+        buf = C.create_string_buffer(256)
+        _check(lib.polar_comm_nvls_info(self.h, C.byref(av), buf, 256), "polar_comm_nvls_info")
+        return bool(av.value), buf.value.decode()
 
 
 def probe_ll128(device=0, pairs=64, iters=20000, jitter_ns=0, jitter_mode=0):

@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     text = open(os.path.join(root, HEADER)).read()
-    declared = set(re.findall(r"^\s*(?:polar_status|uint32_t|uint64_t|const char\*)\s+(polar_\w+)\s*\(", text, re.M))
+    declared = set(re.findall(r"^\s*(?:polar_status|uint32_t|uint64_t|int|const char\*)\s+(polar_\w+)\s*\(", text, re.M))
     assert len(declared) >= 20
     for name in declared:
         assert hasattr(L.lib, name), name

@@ -399,3 +399,32 @@ def test_c3_bf16_1gib_n4_sampled(case):
     finally:
         del ts
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("flags", ["0", "1", "3"])
+def test_ring_tma_forced(flags, monkeypatch):
+    """The TMA-staged ring Simple (kernels.cuh ring_simple_tma; opt-in with
+    POLAR_RING_TMA=1): every dtype / op, several laps and tiles, bf16 f32
+    partials through the FIFO, ragged (non-TMA-eligible) counts falling back to
+    the LDG ring on the same FIFOs, back to back without host sync.  flags: bit 0
+    L2 eviction hints, bit 1 discard of consumed FIFO lines."""
+    monkeypatch.setenv("POLAR_RING_TMA", "1")
+    monkeypatch.setenv("POLAR_RING_TMA_FLAGS", flags)
+    for n in (2, 3, 8):
+        c = L.Comm.virtual(n, 0)
+        try:
+            pending = []
+            for dtype in synth.DTYPES:
+                for op in ("sum", "max"):
+                    for count, nch in ((4096, 1), (3 << 20, 8), (1_000_003, 5), (777_216, 32)):
+                        xs = synth.gen_ranks(dtype, count, n, cfg=14, dist=default_dist(dtype))
+                        ts = [to_device(x, dtype) for x in xs]
+                        c.allreduce_forced(ts, "ring", "simple", nch, op=op)
+                        pending.append((xs, ts, dtype, op))
+                torch.cuda.synchronize()
+                c.check()
+                for xs, ts, dt, op in pending:
+                    check_result([to_host(t, dt) for t in ts], xs, dt, op, "ring", n)
+                pending = []
+        finally:
+            c.destroy()
