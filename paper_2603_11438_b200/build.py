@@ -79,13 +79,35 @@ def build(verbose: bool = True, force: bool = False, defines=(), lib=None, build
             list(ex.map(lambda s: _compile(s, verbose), todo))
     objs = [_obj(s) for s in srcs]
     if force or todo or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread",
+                                                              "-Xlinker", "-soname=libpolar.so"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         if verbose:
             print(f"[build] linked {LIB}", file=sys.stderr)
+    if LIB == os.path.join(PKG, "libpolar.so"):
+        build_tuner(verbose, force)
     return LIB
+
+
+TUNER_SRC = os.path.join(CSRC, "nccl_tuner", "tuner.cpp")
+TUNER_LIB = os.path.join(PKG, "libpolar_nccl_tuner.so")
+
+
+def build_tuner(verbose: bool = True, force: bool = False) -> str:
+    """The NCCL tuner-plugin shim (csrc/nccl_tuner/tuner.cpp): a host-only .so
+    that links libpolar.so (rpath $ORIGIN) and exports ncclTunerPlugin_v3/_v4."""
+    if force or _stale(TUNER_LIB, [TUNER_SRC, LIB, os.path.join(INCLUDE, "polar.h")]):
+        cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-fvisibility=hidden", "-I", INCLUDE,
+               "-I", "/usr/local/cuda/include", TUNER_SRC, "-o", TUNER_LIB, "-L", PKG, "-l:libpolar.so",
+               "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"tuner build failed:\n{r.stderr}")
+        if verbose:
+            print(f"[build] linked {TUNER_LIB}", file=sys.stderr)
+    return TUNER_LIB
 
 
 if __name__ == "__main__":
