@@ -330,9 +330,15 @@ def run_polar(args):
 
         comm = L.Comm.init(ws, rank, local, allgather)
         n = ws
+        # LL128's premise over this transport (a real comm refuses LL128 until it passed)
+        t0 = time.perf_counter()
+        torn, reads = comm.probe_ll128(iters=2000)
+        ll128_probe = {"torn_lanes": torn, "lane_reads": reads, "accepted": torn == 0 and reads > 0,
+                       "s": round(time.perf_counter() - t0, 3)}
     else:
         comm = L.Comm.virtual(VIRTUAL_RANKS, local)
         n = VIRTUAL_RANKS
+        ll128_probe = None
 
         def allgather(b):
             return [b]
@@ -394,6 +400,31 @@ def run_polar(args):
 
     # the timed buffers, re-filled, one more step of the same configuration, checked
     parity = check_parity(L, comm, bufs, host_inputs, ranks_here, n, count, step, allgather)
+
+    # real comms: the north_star call on an UNREGISTERED torch tensor of the same
+    # size (two-shot through the pipelined bounce region) against the registered
+    # buffers timed above
+    unreg = None
+    if real:
+        plain = torch.from_numpy(host_inputs[0]).cuda()
+        pp = [plain.data_ptr()]
+
+        def ustep():
+            st = comm.allreduce_raw(pp, count, L.FLOAT32, L.SUM, sptr)
+            if st != 0:
+                raise L.PolarError(st, "polar_allreduce (unregistered)")
+        for _ in range(args.warmup):
+            ustep()
+        torch.cuda.synchronize()
+        barrier()
+        uk = max(5, min(args.steps, 50))
+        tu = max_over_ranks(_time_calls(ustep, uk, stream))
+        comm.check()
+        unreg = {"busbw_gbs": round(busbw(S_BYTES, n, tu), 2), "us": round(tu * 1e6, 1), "steps": uk,
+                 "ratio_vs_registered": round(tu / t_step, 4),
+                 "path": "torch tensor, not registered: two-shot via the bounce region, copy-in / kernel / copy-out "
+                         "pipelined over 2 x POLAR_BOUNCE/2 halves"}
+        del plain
 
     # roofline of the (only) kernel of the step: the dispatched allreduce kernel
     peak, peak_src = load_peaks()
@@ -496,6 +527,10 @@ def run_polar(args):
             "clocks": clocks.summary(), ("nvlink_sweep" if real else "c2_sweep"): sweep,
             "decision_cost_ns": decision_cost(L), "p2p_probe": probe_out,
         }
+        if ll128_probe is not None:
+            out["ll128_probe"] = ll128_probe
+        if unreg is not None:
+            out["unregistered"] = unreg
         if real and sweep.get("nccl_version"):
             nd = sweep["sizes"].get(str(S_BYTES), {})
             if nd.get("nccl_busbw_gbs"):
@@ -656,7 +691,7 @@ def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, a
             barrier()
             t = max_over_ranks(_time_calls(lambda: polar_call(cnt), it, stream))
             d = comm.last_decision()
-            rec[f"{name}_busbw_gbs"] = round(busbw(sz, n, t), 2)
+            rec[f"{name}_busbw_gbs"] = round(busbw(sz, n, t), 4)
             rec[f"{name}_us"] = round(t * 1e6, 2)
             rec[f"{name}_decision"] = [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels]
         L.set_policy(prev_rows)
@@ -670,10 +705,10 @@ def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, a
             it = int(max(5, min(200, 2e-3 / max(t1, 1e-7))))
             barrier()
             t = max_over_ranks(_time_calls(nccl_call, it, stream))
-            rec["nccl_busbw_gbs"] = round(busbw(sz, n, t), 2)
+            rec["nccl_busbw_gbs"] = round(busbw(sz, n, t), 4)
             rec["nccl_us"] = round(t * 1e6, 2)
             rec["speedup_vs_nccl"] = round(rec["polar_busbw_gbs"] / rec["nccl_busbw_gbs"], 4)
-        rec["nvlink_frac"] = round(rec["polar_busbw_gbs"] / NVLINK_GBS, 4)
+        rec["nvlink_frac"] = round(rec["polar_busbw_gbs"] / NVLINK_GBS, 6)
         out[str(sz)] = rec
     comm.check()
     if nccl is not None:

@@ -257,9 +257,13 @@ polar_status polar_deregister(polar_comm_t comm, void* buf);
 /* In-place AllReduce of `count` elements at device pointer `buf` (real comm,
  * nlocal == 1).  Decides (hook above), then launches ONE kernel on `stream`.
  * count == 0 or nranks == 1 -> POLAR_OK without a launch.  buf need not be
- * 16-B aligned (a scalar path is used) nor registered (two-shot then bounces
- * through the symmetric scratch).  NULL buf with count > 0, bad dtype/op ->
- * POLAR_EINVAL.  Result: every rank holds the rank-ordered reduction
+ * 16-B aligned (a scalar path is used) nor registered: an unregistered buffer
+ * under two-shot travels through the symmetric bounce region (POLAR_BOUNCE,
+ * default 2 x 32 MiB) in chunks whose copy-in (library stream), kernel (this
+ * stream) and copy-out (library stream) overlap; `stream` waits for the last
+ * copy-out.  NULL buf with count > 0, bad dtype/op -> POLAR_EINVAL; an LL128
+ * decision before polar_comm_probe_ll128 passed, or NVLS without a multicast
+ * object -> POLAR_EUNSUPPORTED.  Result: every rank holds the rank-ordered reduction
  * (SURVEY.md §8(c)), bitwise identical on every rank. */
 polar_status polar_allreduce(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype,
                              polar_op op, void* stream);
@@ -428,6 +432,18 @@ const char* polar_status_string(polar_status s);
  * Synchronous; allocates and frees its own device memory.  Diagnostic only. */
 polar_status polar_probe_ll128(int cuda_device, int pairs, unsigned long long iters, unsigned jitter_ns,
                                int jitter_mode, unsigned long long* torn_lanes, unsigned long long* lane_reads);
+
+/* The same LL128 premise over a comm's OWN transport (collective; VERDICT r01
+ * #6): rank r's 64 writer warps stream `iters` LL128 line groups each into rank
+ * (r+1)'s scratch through the peer mapping (CUDA IPC / NVLink), rank (r+1)'s
+ * reader warps poll them in place and return credits through the peer mapping.
+ * *torn_lanes / *lane_reads are summed over every rank.  A real comm accepts
+ * LL128 decisions (policy or forced) only after a probe found 0 torn lanes in
+ * all n x 64 x iters x 32 lane reads (or with POLAR_LL128_REAL=1); until then
+ * they return POLAR_EUNSUPPORTED.  Virtual comms run polar_probe_ll128 on their
+ * device instead.  Synchronous; every wait bounded (POLAR_ETIMEOUT). */
+polar_status polar_comm_probe_ll128(polar_comm_t comm, unsigned long long iters, unsigned long long* torn_lanes,
+                                   unsigned long long* lane_reads);
 
 /* p2p probe (§8(d) "measure it with p2p_probe, no number
  * is assumed"): the empirical peer-path roofline.  COLLECTIVE over the comm.

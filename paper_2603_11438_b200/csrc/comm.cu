@@ -76,8 +76,10 @@ Layout make_layout(bool with_bounce) {
     L.ring128_off = off; off = align_up(off + (size_t)kMaxCh * kSteps * L.ring128_slot, 4096);
     L.tree128_slot = align_up(env_size("POLAR_TREE128_SLOT", 64 << 10), 512);
     L.tree128_off = off; off = align_up(off + (size_t)kMaxCh * 3 * kSteps * L.tree128_slot, 4096);
-    L.bounce_bytes = with_bounce ? align_up(env_size("POLAR_BOUNCE", 64 << 20), 4096) : 0;
+    // two halves of 32 MiB: a 128 MiB message pipelines as 4 chunks
+    L.bounce_bytes = with_bounce ? align_up(env_size("POLAR_BOUNCE", 64 << 20), 8192) : 0;
     L.bounce_off = off; off = align_up(off + L.bounce_bytes, 4096);
+    L.probe_off = off; off = align_up(off + probe_ll128_region_bytes(kProbePairs), 4096);
     L.total = off;
     // NVLS: the region bound to the multicast object (real comms; every rank the same)
     L.nvls_bytes = with_bounce ? align_up(env_size("POLAR_NVLS_BYTES", 256 << 20), 2 << 20) : 0;
@@ -144,9 +146,18 @@ struct polar_comm_s {
     unsigned long long timeout_ns = 0;
     // polar_allreduce_host chunk pipeline (created on first use)
     cudaStream_t hs_in = nullptr, hs_out = nullptr;
+    // unregistered two-shot: copy-in / kernel / copy-out pipeline over the two
+    // halves of the bounce region (created on first use)
+    cudaStream_t bs_in = nullptr, bs_out = nullptr;
+    cudaEvent_t be_start = nullptr, be_in[2] = {}, be_k[2] = {}, be_out[2] = {};
     cudaEvent_t he_start = nullptr, he_in = nullptr, he_red = nullptr, he_out = nullptr;
     unsigned long long probe_epoch = 0;  // p2p probe calls (same count on every rank)
     NvlsState nvls;                      // switch reduction (f1): multicast object, if the node has one
+    // LL128 rests on a warp's 128-B line store landing as one unit; a real comm
+    // accepts LL128 only once polar_comm_probe_ll128 found no torn line over its
+    // own transport (or POLAR_LL128_REAL=1 says so); virtual comms: one GPU,
+    // probed by polar_probe_ll128 (profiles/r01_probe_ll128.jsonl)
+    bool ll128_ok = true;
     std::mutex mu;
 };
 
@@ -440,6 +451,10 @@ void destroy_comm(polar_comm_s* c, bool collective) {
     if (c->tel_host) cudaFreeHost(c->tel_host);
     if (c->hs_in) cudaStreamDestroy(c->hs_in);
     if (c->hs_out) cudaStreamDestroy(c->hs_out);
+    if (c->bs_in) cudaStreamDestroy(c->bs_in);
+    if (c->bs_out) cudaStreamDestroy(c->bs_out);
+    for (cudaEvent_t e : {c->be_start, c->be_in[0], c->be_in[1], c->be_k[0], c->be_k[1], c->be_out[0], c->be_out[1]})
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->he_start, c->he_in, c->he_red, c->he_out})
         if (e) cudaEventDestroy(e);
     delete c;
@@ -591,6 +606,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     const void* fn = nvls ? (c->nvls.ok ? nvls_kernel_for(dtype, op) : nullptr)
                           : kernel_for(dtype, op, (int)d.algo, (int)d.proto);
     if (!fn) return POLAR_EUNSUPPORTED;
+    if (d.proto == POLAR_PROTO_LL128 && !c->ll128_ok) return POLAR_EUNSUPPORTED;   // premise not probed here
     c->last = d;                      // the policy's decision (what the hook returned)
     const bool adaptive_row = (d.flags & POLAR_ROW_ADAPTIVE_NCH) && count > 0 && c->nranks > 1;
     if (c->ad.prm.enabled && count > 0 && c->nranks > 1) {
@@ -691,20 +707,50 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
                               ((uint64_t)(reg->id + 1) << 40) ^ (uint64_t)off);
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
-    // unregistered: bounce through the symmetric scratch, chunk by chunk
-    const size_t chunk_elems = std::max<size_t>(1, (c->L.bounce_bytes / es) & ~(size_t)7);
-    for (int p = 0; p < c->nranks; ++p) P.bufs[p] = c->scratch[p] + c->L.bounce_off;
-    P.vec = 1;   // the bounce region is 16-B aligned on every rank
-    for (size_t done = 0; done < count; done += chunk_elems) {
+    // Unregistered buffer: its peers cannot address it, so it travels through
+    // the symmetric bounce region, split in two halves that alternate by chunk.
+    // Copy-in of chunk k+1 (library stream bs_in), the two-shot kernel of chunk
+    // k (the caller's stream) and copy-out of chunk k-1 (bs_out) overlap; over
+    // NVLink the local copies hide behind the NVLink-bound kernel.  Half h is
+    // refilled only after the copy-out of the chunk before (which followed its
+    // kernel, whose exit barrier means no peer still reads it).  The caller's
+    // stream waits for the last copy-out, so stream order is kept for the user.
+    if (!c->bs_in) {
+        CU_TRY(cudaStreamCreateWithFlags(&c->bs_in, cudaStreamNonBlocking));
+        CU_TRY(cudaStreamCreateWithFlags(&c->bs_out, cudaStreamNonBlocking));
+        CU_TRY(cudaEventCreateWithFlags(&c->be_start, cudaEventDisableTiming));
+        for (int h = 0; h < 2; ++h) {
+            CU_TRY(cudaEventCreateWithFlags(&c->be_in[h], cudaEventDisableTiming));
+            CU_TRY(cudaEventCreateWithFlags(&c->be_k[h], cudaEventDisableTiming));
+            CU_TRY(cudaEventCreateWithFlags(&c->be_out[h], cudaEventDisableTiming));
+        }
+    }
+    const size_t half = (c->L.bounce_bytes / 2) & ~(size_t)15;
+    const size_t chunk_elems = std::max<size_t>(16 / es, (half / es) / (16 / es) * (16 / es));
+    P.vec = 1;   // the bounce halves are 16-B aligned on every rank
+    CU_TRY(cudaEventRecord(c->be_start, stream));
+    CU_TRY(cudaStreamWaitEvent(c->bs_in, c->be_start, 0));
+    CU_TRY(cudaStreamWaitEvent(c->bs_out, c->be_start, 0));
+    size_t k = 0;
+    for (size_t done = 0; done < count; done += chunk_elems, ++k) {
+        const int h = (int)(k & 1);
         const size_t n = std::min(chunk_elems, count - done);
         char* src = mine + done * es;
-        CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, stream));
+        for (int p = 0; p < c->nranks; ++p) P.bufs[p] = c->scratch[p] + c->L.bounce_off + (size_t)h * half;
+        if (k >= 2) CU_TRY(cudaStreamWaitEvent(c->bs_in, c->be_out[h], 0));   // half h is free again
+        CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, c->bs_in));
+        CU_TRY(cudaEventRecord(c->be_in[h], c->bs_in));
+        CU_TRY(cudaStreamWaitEvent(stream, c->be_in[h], 0));
         P.count = n;
         P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, n, 0, kPathBounce);
         st = launch_kernel(c, fn, P, grid, stream, smem);
         if (st != POLAR_OK) return st;
-        CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, stream));
+        CU_TRY(cudaEventRecord(c->be_k[h], stream));
+        CU_TRY(cudaStreamWaitEvent(c->bs_out, c->be_k[h], 0));
+        CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, c->bs_out));
+        CU_TRY(cudaEventRecord(c->be_out[h], c->bs_out));
     }
+    CU_TRY(cudaStreamWaitEvent(stream, c->be_out[(k - 1) & 1], 0));   // bs_out is in order: the last covers all
     return POLAR_OK;
 }
 
@@ -807,6 +853,10 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     c->ag = ag;
     c->user = user;
     c->L = make_layout(true);
+    {
+        const char* e = std::getenv("POLAR_LL128_REAL");
+        c->ll128_ok = e && e[0] == '1';
+    }
     DeviceGuard dg(cuda_device);
     polar_status st = dg.ok ? POLAR_OK : POLAR_ECUDA;
     if (st == POLAR_OK) st = alloc_common(c);
@@ -1112,6 +1162,60 @@ polar_status polar_allreduce_host(polar_comm_t comm, void* const* host_bufs, voi
     CU_TRY(cudaStreamWaitEvent(s, comm->he_out, 0));
     CU_TRY(cudaStreamSynchronize(s));
     return check_latched(comm);
+}
+
+polar_status polar_comm_probe_ll128(polar_comm_t comm, unsigned long long iters, unsigned long long* torn_lanes,
+                                   unsigned long long* lane_reads) {
+    if (!comm || iters < 1 || !torn_lanes || !lane_reads) return POLAR_EINVAL;
+    polar_status st = check_latched(comm);
+    if (st != POLAR_OK) return st;
+    if (comm->is_virtual || comm->nranks == 1) {
+        // one device: the single-GPU probe is the transport's probe
+        st = polar_probe_ll128(comm->device, kProbePairs, iters, 0, 0, torn_lanes, lane_reads);
+        if (st == POLAR_OK) comm->ll128_ok = *torn_lanes == 0 && *lane_reads > 0;
+        return st;
+    }
+    DeviceGuard dg(comm->device);
+    if (!dg.ok) return POLAR_ECUDA;
+    const int r = comm->rank0, n = comm->nranks, next = (r + 1) % n, prev = (r + n - 1) % n;
+    const size_t fifo_bytes = (size_t)kProbePairs * 8 * 512;
+    char* mine = comm->scratch[r] + comm->L.probe_off;
+    unsigned long long* cnt = nullptr;
+    CU_TRY(cudaDeviceSynchronize());
+    if (cudaMalloc(&cnt, 16) != cudaSuccess) return POLAR_ENOMEM;
+    st = cuerr(cudaMemset(mine, 0, probe_ll128_region_bytes(kProbePairs)));
+    if (st == POLAR_OK) st = cuerr(cudaMemset(cnt, 0, 16));
+    if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
+    if (st == POLAR_OK) st = host_barrier(comm);   // every region zeroed before anyone writes
+    if (st == POLAR_OK) {
+        char* to = comm->scratch[next] + comm->L.probe_off;
+        char* from = comm->scratch[prev] + comm->L.probe_off;
+        st = cuerr(launch_probe_ll128_xrank(reinterpret_cast<uint4*>(to),
+                                            reinterpret_cast<unsigned long long*>(mine + fifo_bytes),
+                                            reinterpret_cast<uint4*>(mine),
+                                            reinterpret_cast<unsigned long long*>(from + fifo_bytes), kProbePairs,
+                                            iters, cnt, comm->timeout_ns, comm->err_dev));
+    }
+    if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
+    unsigned long long h[2] = {0, 0};
+    if (st == POLAR_OK) st = cuerr(cudaMemcpy(h, cnt, 16, cudaMemcpyDeviceToHost));
+    cudaFree(cnt);
+    if (st == POLAR_OK) st = check_latched(comm);
+    // every rank learns every rank's count: the gate opens on all ranks or none
+    struct Rec { unsigned long long torn, reads; int32_t st, pad; } me{h[0], h[1], (int32_t)st, 0};
+    std::vector<Rec> all(n);
+    if (comm->ag(&me, all.data(), sizeof(Rec), comm->user) != 0) return POLAR_ESTATE;
+    unsigned long long torn = 0, reads = 0;
+    bool ok = true;
+    for (const Rec& x : all) {
+        torn += x.torn;
+        reads += x.reads;
+        ok = ok && x.st == POLAR_OK;
+    }
+    *torn_lanes = torn;
+    *lane_reads = reads;
+    comm->ll128_ok = ok && torn == 0 && reads == (unsigned long long)n * kProbePairs * iters * 32;
+    return st != POLAR_OK ? st : (ok ? POLAR_OK : POLAR_ESTATE);
 }
 
 polar_status polar_comm_nvls_info(polar_comm_t comm, int* available, char* why, size_t len) {

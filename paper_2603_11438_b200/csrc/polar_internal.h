@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "polar.h"
 
 namespace polar {
@@ -69,6 +71,7 @@ struct Layout {
     size_t ring128_off, ring128_slot; // ring LL128 FIFO: [kMaxCh][kSteps][ring128_slot] (wire bytes)
     size_t tree128_off, tree128_slot; // tree LL128: up [kMaxCh][2][kSteps], down [kMaxCh][kSteps]
     size_t bounce_off, bounce_bytes;  // two-shot bounce for unregistered buffers (real comms)
+    size_t probe_off;                 // LL128 premise probe across ranks (probe_ll128_region_bytes)
     size_t total;
     size_t nvls_bytes;                // NVLS region per rank (POLAR_NVLS_BYTES; 0 = NVLS off), not in scratch
 };
@@ -78,6 +81,14 @@ struct Layout {
 constexpr int kSteps = POLAR_FIFO_STEPS;  // FIFO depth (slots) per connection
 
 Layout make_layout(bool with_bounce);
+
+// LL128 premise over a comm's transport (probe.cu): kProbePairs writer/reader
+// warp pairs; region = FIFO (pairs x 8 line groups) + credits (pairs x 128 B)
+constexpr int kProbePairs = 64;
+size_t probe_ll128_region_bytes(int pairs);
+cudaError_t launch_probe_ll128_xrank(uint4* fifo_out, unsigned long long* credit_in, uint4* fifo_in,
+                                     unsigned long long* credit_out, int pairs, unsigned long long iters,
+                                     unsigned long long* cnt, unsigned long long timeout_ns, int* err);
 
 // ------------------------------------------------------- NVLS (f1, nvls_host.cpp)
 struct NvlsState {

@@ -128,3 +128,89 @@ extern "C" polar_status polar_probe_ll128(int cuda_device, int pairs, unsigned l
     if (prev >= 0) cudaSetDevice(prev);
     return st;
 }
+
+// ------------------------------------------------------------------ across ranks
+// The same premise over a comm's transport: rank r's writer
+// warps stream LL128 line groups into rank (r+1)'s probe FIFO through the peer
+// mapping (CUDA IPC; NVLink on a node), rank (r+1)'s reader warps poll them in
+// their own memory and return credits through the peer mapping.  Blocks
+// [0, pairs) write to the next rank, [pairs, 2 pairs) read from the previous
+// one.  Every spin is bounded (timeout latches into *err and ends the probe).
+namespace polar {
+namespace dev {
+
+__global__ void probe_ll128_xrank_kernel(uint4* fifo_out, unsigned long long* credit_in, uint4* fifo_in,
+                                         unsigned long long* credit_out, int pairs, unsigned long long iters,
+                                         unsigned long long* cnt, unsigned long long timeout_ns, int* err) {
+    const bool writer = (int)blockIdx.x < pairs;
+    const int pair = writer ? (int)blockIdx.x : (int)blockIdx.x - pairs;
+    const int lane = threadIdx.x & 31, q = lane & 7;
+    uint4* base = (writer ? fifo_out : fifo_in) + (size_t)pair * kProbeSlots * 32;
+    unsigned long long* credit = (writer ? credit_in : credit_out) + (size_t)pair * 16;
+    unsigned long long bad = 0, nread = 0;
+    const uint64_t t0 = globaltimer();
+    bool dead = false;
+    for (unsigned long long s = 1; s <= iters && !dead; ++s) {
+        uint4* g = base + (s % kProbeSlots) * 32;
+        if (writer) {
+            if (s > kProbeSlots) {
+                for (uint32_t it = 0;; ++it) {
+                    unsigned long long c;
+                    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(c) : "l"(credit) : "memory");
+                    if (__all_sync(0xffffffffu, c >= s - kProbeSlots)) break;
+                    if ((it & 1023) == 1023 && __any_sync(0xffffffffu, globaltimer() - t0 > timeout_ns || *(volatile int*)err)) {
+                        dead = true;
+                        break;
+                    }
+                }
+                if (dead) break;
+            }
+            const uint32_t pk = (uint32_t)(s * 131u + (unsigned)(lane < 30 ? lane : 0));
+            __syncwarp();
+            st_ll128(g, make_uint4(pk, pk, pk, pk), s);
+        } else {
+            uint4 w;
+            const uint32_t flo = (uint32_t)s, fhi = (uint32_t)(s >> 32);
+            for (uint32_t it = 0;; ++it) {
+                w = ld_ll(g + lane);
+                const bool mine = q != 7 || (w.z == flo && w.w == fhi);
+                if (__all_sync(0xffffffffu, mine)) break;
+                if ((it & 1023) == 1023 && __any_sync(0xffffffffu, globaltimer() - t0 > timeout_ns || *(volatile int*)err)) {
+                    dead = true;
+                    break;
+                }
+            }
+            if (dead) break;
+            const int gi = lane >> 3;
+            const uint32_t pk = (uint32_t)(s * 131u + (unsigned)(q < 7 ? gi * 7 + q : 28 + (gi >> 1)));
+            bool ok = w.x == pk && w.y == pk;
+            if (q < 7) ok = ok && w.z == pk && w.w == pk;
+            bad += ok ? 0 : 1;
+            nread += 1;
+            __syncwarp();
+            if (lane == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(credit), "l"(s) : "memory");
+        }
+    }
+    if (dead && lane == 0) {
+        *(volatile int*)err = POLAR_ETIMEOUT;
+        __threadfence_system();
+    }
+    if (!writer) {
+        atomicAdd(cnt, bad);
+        atomicAdd(cnt + 1, nread);
+    }
+}
+
+}  // namespace dev
+
+cudaError_t launch_probe_ll128_xrank(uint4* fifo_out, unsigned long long* credit_in, uint4* fifo_in,
+                                     unsigned long long* credit_out, int pairs, unsigned long long iters,
+                                     unsigned long long* cnt, unsigned long long timeout_ns, int* err) {
+    dev::probe_ll128_xrank_kernel<<<2 * pairs, 32>>>(fifo_out, credit_in, fifo_in, credit_out, pairs, iters, cnt,
+                                                     timeout_ns, err);
+    return cudaGetLastError();
+}
+
+size_t probe_ll128_region_bytes(int pairs) { return (size_t)pairs * dev::kProbeSlots * 512 + (size_t)pairs * 128; }
+
+}  // namespace polar

@@ -137,6 +137,7 @@ _sigs = {
     "polar_adaptive_simulate": (C.c_int, [C.POINTER(AdaptiveParams), C.c_uint32, C.POINTER(C.c_double), C.c_uint32,
                                           C.POINTER(C.c_uint32)]),
     "polar_nvls_available": (C.c_int, []),
+    "polar_comm_probe_ll128": (C.c_int, [_P, C.c_ulonglong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "polar_comm_nvls_info": (C.c_int, [_P, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     "polar_status_string": (C.c_char_p, [C.c_int]),
     "polar_version": (C.c_char_p, []),
@@ -488,6 +489,14 @@ class Comm:
 
     def check(self):
         _check(lib.polar_comm_check(self.h), "polar_comm_check")
+
+    def probe_ll128(self, iters=2000):
+        """Collective LL128 premise probe over this comm's transport: (torn, reads)
+        summed over ranks; a real comm accepts LL128 only after 0 torn lanes."""
+        torn, reads = C.c_ulonglong(0), C.c_ulonglong(0)
+        _check(lib.polar_comm_probe_ll128(self.h, int(iters), C.byref(torn), C.byref(reads)),
+               "polar_comm_probe_ll128")
+        return torn.value, reads.value
 
     def nvls_info(self):
         """(available, why): does this comm hold a multicast object (NVLS), and

@@ -12,11 +12,11 @@ export POLAR_BENCH_SHARE_GPU=1 POLAR_TIMEOUT_MS=20000
 for n in ${@:-2 4 8}; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
     --master-port $((29500 + n)) bench.py --gpus $n --steps 50 --warmup 5 --policy policies/mps_cap16.json \
-    > gpurun_out/mps_bench_$n.json 2> gpurun_out/mps_bench_$n.err
+    > gpurun_out/mps_bench_$n${TAG:-}.json 2> gpurun_out/mps_bench_$n${TAG:-}.err
   echo "n=$n rc=$?"
   python -c "
 import json
-d=json.load(open('gpurun_out/mps_bench_$n.json'))
-print({k: d[k] for k in ('value','ms_per_step','n_gpus')}, d['decision'], d['roofline']['hbm']['frac'], d['p2p_probe'], d['c2_sweep']['4194304'])" 2>&1 | tail -2
+d=json.loads([l for l in open('gpurun_out/mps_bench_$n${TAG:-}.json') if l.startswith('{')][0])
+print({k: d[k] for k in ('value','ms_per_step','n_gpus')}, d['decision'], d['roofline']['hbm']['frac'], d['p2p_probe'], d.get('unregistered'), d['parity']['ok'])" 2>&1 | tail -2
 done
 echo quit | nvidia-cuda-mps-control

@@ -42,6 +42,15 @@ def main():
 
     comm = L.Comm.init(ws, rank, dev, allgather)
     results = []
+    # LL128 is refused on a real comm until its premise was probed over this transport
+    try:
+        comm.allreduce_forced(torch.ones(4096, device="cuda"), "ring", "ll128", 1)
+        refused = False
+    except L.PolarError as e:
+        refused = e.name == "eunsupported"
+    torn, reads = comm.probe_ll128(iters=2000)
+    results.append({"tag": "ll128-gate", "rank": rank, "ok": refused and torn == 0 and reads == ws * 64 * 2000 * 32,
+                    "identical": True, "torn": torn, "reads": reads})
 
     def check(tag, t, xs, dtype, op, exact):
         got = to_host(t, dtype)
