@@ -663,13 +663,21 @@ def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, a
             nccl, version = None, f"unavailable: {e}"
     prev_rows, _ = L.get_policy()
     tuned_path = os.path.join(ROOT, "policies", f"b200_nvlink{n}.json")
-    tuned = None
+    tuned = single = None
     if os.path.exists(tuned_path):
         with open(tuned_path) as f:
-            tuned = [tuple(r) for r in json.load(f)["rows"]]
+            doc = json.load(f)
+        tuned = [tuple(r) for r in doc["rows"]]
+        if doc.get("best_single"):
+            a_, p_, c_ = doc["best_single"]
+            single = [(0, 0, U64_MAX, L.ALGO_CODES[a_], L.PROTO_CODES[p_], int(c_))]
+    # the paper's comparison points: the active table, bad_channels (E11, PAPER.md
+    # L581-583), the measured per-size table and the best single global choice (E10, L566-568)
     variants = [("polar", prev_rows), ("bad_channels", [(0, 0, U64_MAX, L.UNSET, L.UNSET, 1)])]
     if tuned:
         variants.append(("tuned", tuned))
+    if single:
+        variants.append(("best_single", single))
 
     def polar_call(cnt):
         st = comm.allreduce_raw([ptr], cnt, L.FLOAT32, L.SUM, sptr)

@@ -76,3 +76,19 @@ def test_bench_single_gpu_line():
     assert d["roofline"]["bound"] == "hbm" and d["gpu_launches"] == 5
     for sz, rec in d["c2_sweep"].items():
         assert rec["l2"].startswith("flushed") == (8 * int(sz) <= 2 * (126 << 20))
+
+
+def test_nccl_variants_script():
+    """scripts/nccl_variants.py: every rank on one GPU -> each variant reports a
+    clean skip; one rank -> the ctypes NCCL path runs end to end (its TUNING
+    log parsed) on this box."""
+    r = subprocess.run([sys.executable, "scripts/nccl_variants.py", "--gpus", "2", "--variants", "default,Ring/LL",
+                        "--sizes", "4096,1048576"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    recs = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert [x["variant"] for x in recs] == ["default", "Ring/LL"] and all("share a GPU" in x["skipped"] for x in recs)
+    r = subprocess.run([sys.executable, "scripts/nccl_variants.py", "--gpus", "1", "--variants", "default",
+                        "--sizes", "4096,1048576"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    recs = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(recs) == 2 and all(x["us"] > 0 and x["nccl_version"].startswith("2.") for x in recs), recs

@@ -77,3 +77,21 @@ def test_multiprocess_north_star_size_c2(tmp_path):
     assert dec["c2/unregistered/policy"][:2] == ["twoshot", "simple"]
     # R2 headroom of the f32 ring / tree results (reported, asserted <= 1 above)
     print({x["tag"]: round(x["max_err_over_bound"], 4) for x in res if x["rank"] == 0 and "max_err_over_bound" in x})
+
+
+def test_tune_policy_real_ranks(tmp_path):
+    """scripts/tune_policy.py --real: one process per rank,
+    device time max over ranks, identical call counts on every rank; writes a
+    table polar_set_policy accepts, with the best single choice (E10)."""
+    out = tmp_path / "tuned.json"
+    env = dict(os.environ, POLAR_TIMEOUT_MS="60000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "scripts", "tune_policy.py"),
+           "--real", "--sizes", "4096,262144", "--nch", "2,4", "--combos", "oneshot/ll,twoshot/simple,ring/ll128",
+           "--out", str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    doc = json.loads(out.read_text())
+    assert doc["set_policy_status"] == "ok" and doc["rows"][-1][2] == 2**64 - 1
+    assert doc["best_single"] and doc["ll128_probe"]["torn_lanes"] == 0
+    assert set(doc["winners"]) == {"4096", "262144"}
