@@ -386,11 +386,13 @@ def run_polar(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = comm.launches()
     with ClockSampler(local) as clocks:
+        torch.cuda.nvtx.range_push("timed")     # ncu --nvtx --nvtx-include "timed/": the timed launches only
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         ev1.synchronize()
+        torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     barrier()
     comm.check()

@@ -22,6 +22,10 @@ for w in $WHAT; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 20 --warmup 3 > gpurun_out/ncu_launch_bench_$TAG.log 2>&1
       echo "ncu launches rc=$?"
+      # the timed region only (NVTX range "timed" in bench.py): the step's kernels and their shares
+      timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches_timed_$TAG.csv python bench.py --steps 20 --warmup 3 > gpurun_out/ncu_launch_timed_$TAG.log 2>&1
+      echo "ncu timed launches rc=$?"
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:allreduce_kernel -s 5 -c 1 \
         -f -o gpurun_out/prof_$TAG python bench.py --steps 8 --warmup 3 > gpurun_out/ncu_full_$TAG.log 2>&1
       echo "ncu full rc=$?" ;;

@@ -32,8 +32,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"]
 
 
-def launch_shares(tag):
-    src = os.path.join(OUT, f"launches_{tag}.csv")
+def launch_shares(tag, kind=""):
+    """kind "" = the whole bench run; "timed" = the NVTX "timed" range only."""
+    src = os.path.join(OUT, f"launches_{kind + '_' if kind else ''}{tag}.csv")
+    if not os.path.exists(src):
+        return
     rows = list(csv.reader(open(src)))
     hdr, recs = None, []
     for r in rows:
@@ -48,12 +51,15 @@ def launch_shares(tag):
         agg[k][0] += 1
         agg[k][1] += float(d["Metric Value"])
     tot = sum(v[1] for v in agg.values()) or 1.0
-    lines = [f"# ncu launch list ({src}), gpu__time_duration.sum, --clock-control none (cold, serialised)",
+    what = "the timed region only (NVTX range 'timed')" if kind else "the whole bench.py run"
+    lines = [f"# ncu launch list of {what} ({os.path.basename(src)}), gpu__time_duration.sum, "
+             "--clock-control none (cold, serialised)",
              "# launches  total_us  share  mean_us  kernel grid block"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"{v[0]:8d} {v[1] / 1e3:10.1f} {100 * v[1] / tot:6.1f}% {v[1] / v[0] / 1e3:9.2f}  {k[0]} {k[1]} {k[2]}")
-    shutil.copy(src, os.path.join(PROF, f"{tag}_launches.csv"))
-    with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
+    suffix = f"_{kind}" if kind else ""
+    shutil.copy(src, os.path.join(PROF, f"{tag}_launches{suffix}.csv"))
+    with open(os.path.join(PROF, f"{tag}_launch_shares{suffix}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines[:8]))
 
@@ -101,6 +107,7 @@ def main():
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     launch_shares(a.tag)
+    launch_shares(a.tag, "timed")
     full_metrics(a.tag, a.workload)
 
 
