@@ -103,7 +103,10 @@ def c2():
         d = comm.last_decision()
         rec = {"config": "C2", "n": n, "dtype": "f32", "bytes": size, "policy": "default",
                "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
-               "busbw_gbs": round(busbw(size, n, t), 1), "us": round(t * 1e6, 1)}
+               "busbw_gbs": round(busbw(size, n, t), 1), "us": round(t * 1e6, 1),
+               # back-to-back calls: where the n ranks' buffers fit in the 126 MB L2 the
+               # inputs may be L2-resident (bench.py's c2_sweep flushes instead)
+               "l2_resident_possible": n * size <= (126 << 20)}
         forced = {}
         for algo, proto in ALGOS:
             best = None

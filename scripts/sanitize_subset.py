@@ -41,6 +41,23 @@ torch.cuda.synchronize()
 ok = all(np.array_equal(to_host(t, "f32"), orc.allreduce(xs, "f32", "sum")) for t in ts)
 bad += 0 if ok else 1
 print("tma twoshot", "ok" if ok else "MISMATCH", flush=True)
+# TMA-staged ring Simple (opt-in kernel; round 2), with and without L2 hints + discard
+for flags in ("1", "3"):
+    os.environ["POLAR_RING_TMA"] = "1"
+    os.environ["POLAR_RING_TMA_FLAGS"] = flags
+    cr = L.Comm.virtual(n, 0)
+    for dtype in ("f32", "bf16"):
+        for count in (300_001 * 4 // 4 * 4, 1_300_000):
+            xs = synth.gen_ranks(dtype, count, n, cfg=7, dist="ints")
+            ts = [to_device(x, dtype) for x in xs]
+            cr.allreduce_forced(ts, "ring", "simple", 2)
+            torch.cuda.synchronize()
+            cr.check()
+            ok = all(np.array_equal(to_host(t, dtype), orc.allreduce(xs, dtype, "sum")) for t in ts)
+            bad += 0 if ok else 1
+            print("ring tma", flags, dtype, count, "ok" if ok else "MISMATCH", flush=True)
+    cr.destroy()
+    del os.environ["POLAR_RING_TMA"], os.environ["POLAR_RING_TMA_FLAGS"]
 sends = [torch.randn(n * 1000, device="cuda") for _ in range(n)]
 recvs = [torch.empty(1000, device="cuda") for _ in range(n)]
 c.reduce_scatter(sends, recvs)
