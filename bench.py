@@ -680,6 +680,10 @@ def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, a
         variants.append(("tuned", tuned))
     if single:
         variants.append(("best_single", single))
+    if comm.nvls_info()[0]:
+        # the switch reduction, where the node grants a multicast object (f1; NCCL's
+        # own default on the paper's node)
+        variants.append(("nvls", [(0, 0, U64_MAX, L.NVLS, L.SIMPLE, 32)]))
 
     def polar_call(cnt):
         st = comm.allreduce_raw([ptr], cnt, L.FLOAT32, L.SUM, sptr)

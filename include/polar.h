@@ -219,7 +219,14 @@ polar_status polar_bootstrap_check(int nranks, int rank, polar_allgather_fn ag, 
  * on an otherwise idle GPU; plain launch + programmatic dependent launch like
  * real comms, POLAR_VIRTUAL_COOP=1 forces a cooperative launch).  Same kernels,
  * same protocols; peers are local HBM instead of NVLink (DESIGN.md "Virtual
- * ranks").  Every cross-rank wait is bounded (POLAR_TIMEOUT_MS). */
+ * ranks").  Every cross-rank wait is bounded (POLAR_TIMEOUT_MS).
+ * Concurrency: the launch is plain (not cooperative), sized so that every CTA
+ * is resident on an otherwise idle GPU.  Keep ONE virtual-comm collective in
+ * flight per device at a time: two concurrent grids (two virtual comms, or one
+ * comm on two streams) can each hold SMs the other's spinning CTAs need, which
+ * ends in POLAR_ETIMEOUT (latched) instead of a result.  POLAR_VIRTUAL_COOP=1
+ * makes the launch cooperative (co-residency checked by the runtime, ~2 us more
+ * per call). */
 polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_device);
 
 /* Collective for real comms: synchronises the device, host-barriers through the

@@ -156,3 +156,31 @@ def test_p2p_probe_virtual(n):
         assert (res[r]["pingpong_us"] > 0) == ((r ^ 1) < n)
         got = bufs[peer].cpu().numpy().view(np.uint32)
         assert np.array_equal(got, _pattern(nbytes // 16, r)), r
+
+
+def test_binding_rejects_bad_tensors():
+    """polar.py passes only a pointer and one count per call: a strided view, a
+    buffer shorter than its peers', mixed dtypes, host tensors or a wrong RS/AG
+    size ratio would make a kernel read or write past a buffer's end — the
+    binding refuses them with EINVAL before anything is launched."""
+    n = 2
+    c = comm(n)
+    before = c.launches()
+    good = [torch.zeros(1000, device="cuda") for _ in range(n)]
+    cases = [
+        [torch.zeros(2000, device="cuda")[::2], good[1]],                 # strided view
+        [good[0], torch.zeros(999, device="cuda")],                        # shorter peer
+        [good[0], torch.zeros(1000, device="cuda", dtype=torch.int32)],    # mixed dtype
+        [torch.zeros(1000), good[1]],                                      # host tensor
+    ]
+    for ts in cases:
+        with pytest.raises(L.PolarError) as e:
+            c.allreduce(ts)
+        assert e.value.name == "einval"
+    with pytest.raises(L.PolarError) as e:     # RS: numel(send) must be n * numel(recv)
+        c.reduce_scatter([torch.zeros(1999, device="cuda") for _ in range(n)], good)
+    assert e.value.name == "einval"
+    with pytest.raises(L.PolarError) as e:     # AG: numel(recv) must be n * numel(send)
+        c.all_gather(good, [torch.zeros(1000, device="cuda") for _ in range(n)])
+    assert e.value.name == "einval"
+    assert c.launches() == before
