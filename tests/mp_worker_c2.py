@@ -100,10 +100,13 @@ def main():
     torch.cuda.synchronize()
     comm.check()
     check("c2/unregistered/policy", plain, True)
-    # 3. forced ring / tree Simple on the unregistered tensor (32 channels, the paper's setting)
+    # 3. forced ring / tree Simple on the unregistered tensor (32 channels, the paper's
+    #    setting; POLAR_TEST_NCH lowers it when every rank shares one GPU: 8 x 32 CTAs
+    #    would not be co-resident on 148 SMs)
+    fnch = int(os.environ.get("POLAR_TEST_NCH", "32"))
     for algo in ("ring", "tree"):
         plain.copy_(torch.from_numpy(x_mine))
-        comm.allreduce_forced(plain, algo, "simple", 32)
+        comm.allreduce_forced(plain, algo, "simple", fnch)
         torch.cuda.synchronize()
         comm.check()
         check(f"c2/{algo}/simple/32ch", plain, False)
