@@ -178,8 +178,11 @@ def main():
     # warp-specialised ring and tree Simple (multi-slot), ring LL; every replay
     # advances the device-resident epochs / FIFO counters, none is host-synced
     # between the captured calls
+    # (the last entry: an UNREGISTERED two-shot, i.e. the bounce pipeline with its
+    # two library streams forked into and joined back from the capture, several
+    # chunks with the test's 1 MiB bounce region)
     plan = [("twoshot", "simple", 50_003), ("ring", "simple", 400_001), ("tree", "simple", 1_000_003),
-            ("ring", "ll", 20_011)]
+            ("ring", "ll", 20_011), ("twoshot", "simple", 700_001)]
     (gsym,) = comm.mem_alloc_tensors(plan[0][2], torch.float32)
     gbufs = [gsym] + [torch.empty(c, dtype=torch.float32, device="cuda") for _, _, c in plan[1:]]
     s = torch.cuda.Stream()
@@ -203,6 +206,13 @@ def main():
         for (algo, proto, _), xs, b in zip(plan, xss, gbufs):
             check(f"graph{rep}/{algo}/{proto}", b, xs, "f32", "sum", True)
     del g, gbufs, gsym
+    # the e2e host path on unregistered device buffers (host chunks x bounce chunks)
+    xs = synth.gen_ranks("f32", 900_001, ws, cfg=95, dist="ints")
+    host = torch.from_numpy(xs[rank].copy()).pin_memory()
+    devb = torch.empty(900_001, dtype=torch.float32, device="cuda")
+    comm.allreduce_host(host, devb)
+    comm.check()
+    check("host/unregistered", host, xs, "f32", "sum", True)
     # cross-rank decision check (kernels.cuh tag_begin/tag_end):
     # every call above was consistent, so nothing may have latched; then rank 0
     # alone asks for MAX where the others ask for SUM (same algorithm, count and

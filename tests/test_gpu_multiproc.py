@@ -48,7 +48,7 @@ def test_multiprocess_ipc_all_algorithms(tmp_path, nranks, tma, jitter):
     res = json.loads(out.read_text())
     bad = [x for x in res if not (x["ok"] and x["identical"])]
     assert not bad, bad
-    assert len(res) == nranks * (1 + 4 * 3 * 3 + 3 + 4 + 1 + 1 + 6 + 3 * 4 + 1)
+    assert len(res) == nranks * (1 + 4 * 3 * 3 + 3 + 4 + 1 + 1 + 6 + 3 * 5 + 1 + 1)
 
 
 def test_multiprocess_north_star_size_c2(tmp_path):
