@@ -680,9 +680,11 @@ def nvlink_sweep(args, L, comm, big, n, rank, stream, barrier, max_over_ranks, a
         variants.append(("tuned", tuned))
     if single:
         variants.append(("best_single", single))
-    if comm.nvls_info()[0]:
+    if comm.nvls_info()[0] and os.environ.get("POLAR_BENCH_NVLS") == "1":
         # the switch reduction, where the node grants a multicast object (f1; NCCL's
-        # own default on the paper's node)
+        # own default on the paper's node).  Opt-in: the NVLS
+        # kernels have never run on this pool (no multicast object), and a failing
+        # variant must not cost the rest of the bench line.
         variants.append(("nvls", [(0, 0, U64_MAX, L.NVLS, L.SIMPLE, 32)]))
 
     def polar_call(cnt):
