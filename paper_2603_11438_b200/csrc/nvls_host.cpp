@@ -267,14 +267,14 @@ polar_status nvls_setup(NvlsState& s, int nranks, int rank, int device, polar_al
         acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
         acc.location.id = device;
         acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-        r = d.addrReserve(&uva, s.bytes, s.bytes, 0, 0);
+        r = d.addrReserve(&uva, s.bytes, 0, 0, 0);   // default alignment (the size need not be a power of two)
         if (r != CUDA_SUCCESS) { fail(m, "cuMemAddressReserve", r); goto done; }
         r = d.memMap(uva, s.bytes, 0, ph, 0);
         if (r != CUDA_SUCCESS) { d.addrFree(uva, s.bytes); fail(m, "cuMemMap(unicast)", r); goto done; }
         s.uc = reinterpret_cast<char*>(uva);
         r = d.memSetAccess(uva, s.bytes, &acc, 1);
         if (r != CUDA_SUCCESS) { fail(m, "cuMemSetAccess(unicast)", r); goto done; }
-        r = d.addrReserve(&mva, s.bytes, s.bytes, 0, 0);
+        r = d.addrReserve(&mva, s.bytes, 0, 0, 0);
         if (r != CUDA_SUCCESS) { fail(m, "cuMemAddressReserve", r); goto done; }
         r = d.memMap(mva, s.bytes, 0, (CUmemGenericAllocationHandle)s.mc_handle, 0);
         if (r != CUDA_SUCCESS) { d.addrFree(mva, s.bytes); fail(m, "cuMemMap(multicast)", r); goto done; }
