@@ -162,6 +162,9 @@ ncclResult_t tuner_init(size_t nRanks, size_t nNodes, ncclDebugLogger_t logFunct
         }
     }
     *context = c;
+    if (logFunction)   // NCCL_LOG_INFO (3), subsystem NCCL_INIT (0x1)
+        logFunction(3, 0x1, __FILE__, __LINE__, "polar tuner: init nRanks %zu nNodes %zu, policy %s (generation %u)",
+                    nRanks, nNodes, g_file ? "from POLAR_POLICY" : "libpolar's active table", polar_policy_generation());
     return ncclSuccess;
 }
 
@@ -203,6 +206,9 @@ ncclResult_t tuner_get(void* context, ncclFunc_t collType, size_t nBytes, int, f
                     else if (pa >= 0 && pp >= 0) table[a][p] = 0.0f;   // the one preferred cell
                 }
     }
+    if (c->log)        // NCCL_LOG_INFO (3), subsystem NCCL_TUNING (0x40)
+        c->log(3, 0x40, __FILE__, __LINE__, "polar tuner: coll %d bytes %zu -> row algo %u proto %u nch %u", (int)collType,
+               nBytes, row.algo, row.proto, row.nchannels);
     if (row.nchannels && nChannels) {
         int want = row.nchannels > POLAR_MAXCH ? POLAR_MAXCH : (int)row.nchannels;
         if (*nChannels > 0 && want > *nChannels) want = *nChannels;   // NCCL's maximum

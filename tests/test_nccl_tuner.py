@@ -185,3 +185,18 @@ print("ok")
     env = dict(os.environ, POLAR_POLICY=os.path.join(ROOT, "policies", "nvlink_ring_mid_v2.json"))
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_nccl_loads_the_shim():
+    """NCCL 2.28.9 itself (torch's libnccl.so.2, through ctypes) loads the shim
+    as a tuner plugin and calls its init on a one-rank communicator (the pool has
+    one GPU; NCCL asks a tuner for decisions only on multi-rank communicators)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "experiments", "nccl_tuner_load.py")], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "TUNER/Plugin: Using polar" in r.stdout and "polar tuner: init nRanks 1" in r.stdout
+    assert r.stdout.strip().endswith("LOADED")
