@@ -1,0 +1,561 @@
+// Ring and tree Simple for VIRTUAL comms as thread-block clusters (SURVEY.md §8
+// rows a4, a6, a8, a9; DESIGN.md §8 "Cluster transport").
+//
+// A virtual comm hosts all n ranks on one GPU.  The FIFO kernels (kernels.cuh
+// ring / ring_simple_ws / tree_simple_ws) move every hop through a FIFO in HBM
+// (L2), so on one GPU the ring issues 6n - 4 memory operations of S/n per rank
+// against the two-shot's 2: it is bound by that memory-operation count, not by
+// its wires.  Here the n ranks of one channel are the n CTAs of ONE cluster
+// (cluster rank = rank), and a hop is a distributed-shared-memory store into the
+// receiver's shared-memory inbox:
+//   * the sender's warps write the tile with st.async (16 B per lane) straight
+//     into the receiver's inbox stage; each warp also arrives on the receiver's
+//     `full` mbarrier with the byte count it sent (expect_tx), so the phase
+//     completes exactly when every byte of the tile has landed;
+//   * the receiver's warps read the stage, then arrive on the sender's `empty`
+//     mbarrier (remote arrive, release.cluster): the stage may be rewritten;
+//   * a loader warp streams the rank's own input tiles from HBM into shared
+//     memory with cp.async.bulk (TMA), as far ahead as its stages allow — own
+//     data does not depend on the ring;
+//   * results go to HBM with 16-B stores from registers.
+// HBM then sees each input read once and each output written once: 2 n S per
+// call, the same algorithmic bytes as the two-shot.  The schedule, the chunk
+// geometry and the reduction order are the FIFO ring's / tree's, so for the
+// same channel count the results are bit-identical to the FIFO kernels
+// (GPU test test_cluster_matches_fifo).
+//
+// The cluster's CTAs are co-scheduled by the hardware, so no wait here depends
+// on another launch or on co-residency; every wait is still bounded
+// (POLAR_ETIMEOUT latched, then an orderly exit).  Channels are independent
+// clusters.  Real comms (ranks on different GPUs) keep the FIFO kernels: a
+// cluster cannot span GPUs.
+//
+// Used when every pack is a whole 16-B pack of a 16-B aligned buffer (bulk copies
+// are 16-B granular); otherwise the FIFO kernels run.
+#pragma once
+#include "kernels.cuh"   // npacks, split_range, Acc arithmetic (device.cuh)
+
+namespace polar {
+namespace dev {
+
+#ifndef POLAR_CL_WARPS
+#define POLAR_CL_WARPS 8          // compute warps (warp 0 loads, warp 1 signals)
+#endif
+#ifndef POLAR_CL_STAGES
+#define POLAR_CL_STAGES 10        // ring inbox stages (>= tiles per ring step + slack)
+#endif
+#ifndef POLAR_CL_PROF
+#define POLAR_CL_PROF 0           // diagnostic wait-time counters into P.trace
+#endif
+#ifndef POLAR_CL_OWN
+#define POLAR_CL_OWN 3            // own-input stages (TMA loads in flight)
+#endif
+constexpr int kClWarps = POLAR_CL_WARPS;
+constexpr int kClThreads = 32 * (kClWarps + 2);
+constexpr int kClStages = POLAR_CL_STAGES;
+constexpr int kClOwn = POLAR_CL_OWN;
+#ifndef POLAR_CL_WIRE
+#define POLAR_CL_WIRE 1024        // 16-B wire words per stage (16 KiB)
+#endif
+constexpr unsigned kClWire = POLAR_CL_WIRE;
+constexpr size_t kClStageBytes = (size_t)kClWire * 16;
+// element packs per tile: a tile's wire words fill one stage (bf16: 2 f32 words per pack)
+template <int AW> __host__ __device__ constexpr unsigned cl_tile() { return kClWire / (unsigned)AW; }
+// ring inbox stages needed per ring step + slack for the credit round trip
+constexpr int kClSlack = 4;
+__host__ __device__ constexpr size_t cl_ring_smem_bytes() {
+    return (size_t)(kClStages + kClOwn) * kClStageBytes + (size_t)(3 * kClStages + 2 * kClOwn + 1) * 8;
+}
+
+// ----------------------------------------------------------- cluster primitives
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// this CTA's shared address `a` as seen in cluster CTA `rank`'s shared window
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+#ifndef POLAR_CL_ABL
+#define POLAR_CL_ABL 0            // diagnostic ablation: 2 = no HBM result stores
+#endif
+__device__ __forceinline__ void cl_st_async(uint32_t raddr, uint4 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
+}
+// Remote arrives are RELAXED: a release arrive makes the issuing thread wait
+// until its earlier global stores (the results just written to HBM) are
+// performed at cluster scope, ~1 us per tile on the critical path.  No release
+// is needed: `full` carries its data through st.async's complete_tx, and an
+// `empty` credit follows shared-memory reads whose values were already
+// consumed (stored / sent) by the warp before its __syncwarp.
+#ifndef POLAR_CL_RELEASE
+#define POLAR_CL_RELEASE 0
+#endif
+#if POLAR_CL_RELEASE
+#define POLAR_CL_SEM "release"
+#else
+#define POLAR_CL_SEM "relaxed"
+#endif
+__device__ __forceinline__ void cl_arrive_remote(uint32_t rbar) {
+    asm volatile("mbarrier.arrive." POLAR_CL_SEM ".cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+__device__ __forceinline__ void cl_arrive_expect_remote(uint32_t rbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx." POLAR_CL_SEM ".cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar),
+                 "r"(bytes)
+                 : "memory");
+}
+// POLAR_CL_WAIT: 0 = mbarrier.try_wait (may suspend the thread until the phase
+// completes or a system time limit), 1 = mbarrier.test_wait spin (never
+// suspends), 2 = try_wait with an explicit suspend-time hint (POLAR_CL_HINT ns)
+#ifndef POLAR_CL_WAIT
+#define POLAR_CL_WAIT 0
+#endif
+#ifndef POLAR_CL_HINT
+#define POLAR_CL_HINT 1000
+#endif
+// Waits are acquire.CTA (the default): acquire.cluster compiles to a
+// CCTL.IVALL (whole-L1 invalidation) after every successful wait, which the
+// compute warps paid once per tile.  Nothing here reads global memory that a
+// peer wrote: inbox data arrives through st.async, whose bytes are complete
+// when the mbarrier phase completes (complete_tx), and credits order nothing
+// but shared-memory reuse.
+__device__ __forceinline__ bool cl_try_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+#if POLAR_CL_WAIT == 1
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
+        "p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+#elif POLAR_CL_WAIT == 2
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, "
+        "0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "n"(POLAR_CL_HINT)
+        : "memory");
+#else
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
+        "p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+#endif
+    return ok != 0;
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// Bounded wait for the completion of the phase with parity `parity`.  `honour_err`:
+// give up as soon as another thread latched an error (the final rendezvous
+// waits for its peers regardless, so that no CTA leaves while a peer may still
+// write its shared memory).
+static __device__ __noinline__ bool cl_wait_slow(uint32_t bar, uint32_t parity, unsigned long long timeout_ns, int* err,
+                                                 int honour_err) {
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1;; ++it) {
+        if (cl_try_wait(bar, parity)) return true;
+        if ((it & 63) == 0) {
+            if (globaltimer() - t0 > timeout_ns) {
+                *(volatile int*)err = POLAR_ETIMEOUT;
+                __threadfence_system();
+                return false;
+            }
+            if (honour_err && *(volatile int*)err) return false;
+        }
+    }
+}
+__device__ __forceinline__ bool cl_wait(const Params& P, uint32_t bar, uint32_t parity) {
+    if (cl_try_wait(bar, parity)) return true;
+    return cl_wait_slow(bar, parity, P.timeout_ns, P.err, 1);
+}
+
+// Shared memory of one cluster-ring CTA (dynamic; byte offsets):
+//   inbox [kClStages][kClStageBytes]  written by the predecessor (st.async)
+//   own   [kClOwn][kClStageBytes]     my input tiles (TMA)
+//   full  [kClStages]  inbox stage landed: 1 arrival (my signal warp arms it with
+//                      the tile's byte count) + the predecessor's st.async bytes
+//   cons  [kClStages]  my compute warps have read the stage (kClWarps arrivals)
+//   empty [kClStages]  the successor's stage is free: 1 remote arrival (its
+//                      signal warp, after its cons)
+//   ofull [kClOwn]     own tile landed (1 arrival + tx; loader)
+//   oempty[kClOwn]     own stage free (kClWarps arrivals)
+//   fin                final rendezvous (n - 1 remote arrivals)
+// Inbox words are planar: word q of element pack p of a tile at (q * TP + p) * 16,
+// so a warp's 16-B accesses are contiguous (no 32-B stride bank conflicts).
+// Compute warps only touch local barriers; the one remote arrive per tile (the
+// credit) is the signal warp's, off the data path.
+struct ClRingSmem {
+    uint32_t inbox, own, full, cons, empty, ofull, oempty, fin;
+};
+__device__ __forceinline__ ClRingSmem cl_ring_smem(uint32_t base) {
+    ClRingSmem s;
+    s.inbox = base;
+    s.own = base + (uint32_t)(kClStages * kClStageBytes);
+    s.full = s.own + (uint32_t)(kClOwn * kClStageBytes);
+    s.cons = s.full + 8u * kClStages;
+    s.empty = s.cons + 8u * kClStages;
+    s.ofull = s.empty + 8u * kClStages;
+    s.oempty = s.ofull + 8u * kClOwn;
+    s.fin = s.oempty + 8u * kClOwn;
+    return s;
+}
+__device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive." POLAR_CL_SEM ".cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_u32(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx." POLAR_CL_SEM ".cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load_u32(uint32_t sdst, const void* gsrc, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sdst),
+                 "l"(gsrc), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Final rendezvous: no CTA leaves while a peer may still touch its shared memory
+// (the successor's last credits land on my `empty` barriers after my loop).
+// Thread 0 of each CTA arrives on every peer's `fin` and waits for its own.
+__device__ __forceinline__ void cl_rendezvous(const Params& P, uint32_t fin, int r, int n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < n; ++p)
+            if (p != r) cl_arrive_remote(cl_map(fin, (uint32_t)p));
+        if (!cl_try_wait(fin, 0)) cl_wait_slow(fin, 0, P.timeout_ns, P.err, 0);
+    }
+    __syncthreads();
+}
+
+// The ring schedule of one channel, exactly as kernels.cuh `ring` walks it:
+// laps of n sub-chunks of SP packs; step s of 2(n-1)+1 handles sub-chunk k(s);
+// each sub-chunk in tiles of TP packs.  A resumable cursor, so that the signal
+// warp can walk the received tiles kClStages ahead of its own position.
+struct RingCursor {
+    unsigned long long base, L, ks, ke, i0;
+    int s;
+    bool done;
+};
+__device__ __forceinline__ void ring_cursor_step(RingCursor& q, int r, int n, unsigned long long cb,
+                                                 unsigned long long SP) {
+    // position q at the first tile of step q.s of the lap at q.base (or later)
+    const unsigned long long LC = SP * (unsigned long long)n;
+    for (;;) {
+        if (q.base >= cb) { q.done = true; return; }
+        q.L = (cb - q.base < LC) ? cb - q.base : LC;
+        if (q.s > 2 * (n - 1)) { q.base += LC; q.s = 0; continue; }
+        int k;
+        if (q.s < n) k = ((r - q.s) % n + n) % n;
+        else k = ((r - (q.s - n)) % n + n) % n;
+        if (q.s == n - 1) k = (r + 1) % n;
+        q.ks = q.base + q.L * (unsigned long long)k / n;
+        q.ke = q.base + q.L * (unsigned long long)(k + 1) / n;
+        q.i0 = q.ks;
+        if (q.ks < q.ke) return;
+        ++q.s;   // empty sub-chunk (tiny lap): no tile
+    }
+}
+__device__ __forceinline__ RingCursor ring_cursor(int r, int n, unsigned long long ca, unsigned long long cb,
+                                                  unsigned long long SP) {
+    RingCursor q;
+    q.base = ca;
+    q.s = 0;
+    q.done = false;
+    ring_cursor_step(q, r, n, cb, SP);
+    return q;
+}
+__device__ __forceinline__ unsigned ring_cursor_npk(const RingCursor& q, unsigned TP) {
+    return (unsigned)((q.ke - q.i0) < TP ? (q.ke - q.i0) : TP);
+}
+__device__ __forceinline__ void ring_cursor_next(RingCursor& q, int r, int n, unsigned long long cb,
+                                                 unsigned long long SP, unsigned TP) {
+    q.i0 += TP;
+    if (q.i0 < q.ke) return;
+    ++q.s;
+    ring_cursor_step(q, r, n, cb, SP);
+}
+template <class F>
+__device__ __forceinline__ bool cl_ring_walk(int r, int n, unsigned long long ca, unsigned long long cb,
+                                             unsigned long long SP, unsigned TP, F&& f) {
+    for (RingCursor q = ring_cursor(r, n, ca, cb, SP); !q.done; ring_cursor_next(q, r, n, cb, SP, TP))
+        if (!f(q.s, q.i0, ring_cursor_npk(q, TP))) return false;
+    return true;
+}
+// next RECEIVED tile (steps s >= 1) at or after q
+__device__ __forceinline__ void ring_cursor_recv(RingCursor& q, int r, int n, unsigned long long cb,
+                                                 unsigned long long SP, unsigned TP) {
+    while (!q.done && q.s == 0) ring_cursor_next(q, r, n, cb, SP, TP);
+}
+
+// Sub-chunk size: the FIFO ring's slot (same geometry => same reduction order),
+// capped so that one ring step fits the inbox with kClSlack stages to spare.
+// (Each rank receives a whole step before its successor frees it: a ring step
+// must fit the inbox or the ring deadlocks.)
+template <int AW> __device__ __forceinline__ unsigned long long cl_ring_sp(const Params& P) {
+    const unsigned long long fifo = P.ring_slot / 16 / AW;
+    const unsigned long long cap = (unsigned long long)(kClStages - kClSlack) * cl_tile<AW>();
+    return fifo < cap ? fifo : cap;
+}
+
+// Step kinds of the ring schedule (uniform per step):
+//   first  s = 0        own -> [widen] -> successor              (AW words)
+//   mid    0 < s < n-1  inbox (AW) (op) own -> successor         (AW words)
+//   fin    s = n-1      fin(inbox (op) own) -> HBM + successor  (1 word)
+//   ag     n-1 < s < 2(n-1)   inbox (1) -> HBM + successor
+//   last   s = 2(n-1)   inbox (1) -> HBM
+enum { kClFirst = 0, kClMid = 1, kClFin = 2, kClAg = 3, kClLast = 4 };
+
+// The compute warps' state and per-step tile loop.  Stage indices and phase
+// parities are 32-bit counters that wrap (no 64-bit division per tile); each
+// step kind is its own instantiation, so the per-pack code has no step branches.
+template <int DT, int OP>
+struct ClCompute {
+    static constexpr int AW = AccWords<DT>::N;
+    static constexpr unsigned TP = cl_tile<AW>();
+    static constexpr unsigned NT = kClWarps * 32;             // compute threads
+    static constexpr unsigned PPL = (TP + NT - 1) / NT;       // packs per lane per tile
+    ClRingSmem S;
+    uint32_t dst_inbox, dst_full;
+    uint4* mine;
+    uint32_t me;                                              // compute thread index
+    uint32_t xi = 0, pi = 0;        // inbox stage / parity of the phase to wait for
+    uint32_t xo = 0, pe = 1;        // successor stage / parity of its credit phase
+    uint32_t xw = 0, pw = 0;        // own stage / parity
+    bool wrapped = false;           // sent >= kClStages: credits are needed
+
+    // One tile: every shared-memory load of the lane's PPL packs first, then
+    // the arithmetic, then the stores (one register set per pack: loads of later
+    // packs are not serialised behind the stores of earlier ones).
+    template <int KIND, bool FULL>
+    __device__ __forceinline__ void body(uint32_t in, uint32_t ow, uint32_t dst, uint32_t dbar, uint4* gout,
+                                         unsigned npk) {
+        constexpr bool SEND = KIND != kClLast, OWN = KIND <= kClFin, OUT = KIND >= kClFin;
+        constexpr int WIN = (KIND == kClMid || KIND == kClFin) ? AW : (KIND == kClFirst ? 0 : 1);
+        constexpr int WOUT = KIND <= kClMid ? AW : 1;
+        uint4 o[PPL], a[PPL][AW > 1 ? AW : 1];
+#pragma unroll
+        for (unsigned u = 0; u < PPL; ++u) {
+            const unsigned p = u * NT + me;
+            if (!FULL && p >= npk) continue;
+            if constexpr (OWN) o[u] = ld_shared_v4(ow + p * 16u);
+#pragma unroll
+            for (int q = 0; q < WIN; ++q) a[u][q] = ld_shared_v4(in + ((unsigned)q * TP + p) * 16u);
+        }
+#pragma unroll
+        for (unsigned u = 0; u < PPL; ++u) {
+            const unsigned p = u * NT + me;
+            if (!FULL && p >= npk) continue;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if constexpr (OWN) {
+                Acc<DT> acc;
+                if constexpr (KIND == kClFirst) {
+                    acc_init<DT>(acc, o[u]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) acc.w[q] = a[u][q];
+                    acc_add<DT, OP>(acc, o[u]);
+                }
+                if constexpr (KIND != kClFin) {
+#pragma unroll
+                    for (int q = 0; q < WOUT; ++q) cl_st_async(dst + ((unsigned)q * TP + p) * 16u, acc.w[q], dbar);
+                    continue;
+                } else {
+                    v = acc_fin<DT>(acc);
+                }
+            } else {
+                v = a[u][0];
+            }
+            if constexpr (OUT) {
+                if (POLAR_CL_ABL != 2) st_plain(gout + p, v);
+            }
+            if constexpr (SEND) cl_st_async(dst + p * 16u, v, dbar);
+        }
+    }
+
+    template <int KIND>
+    __device__ __forceinline__ bool tiles(const Params& P, unsigned long long ks, unsigned long long ke) {
+        constexpr bool RECV = KIND != kClFirst, SEND = KIND != kClLast;
+        constexpr bool OWN = KIND <= kClFin;
+        for (unsigned long long i0 = ks; i0 < ke; i0 += TP) {
+            const unsigned npk = (unsigned)((ke - i0) < TP ? (ke - i0) : TP);
+            if (RECV && !cl_wait(P, S.full + 8u * xi, pi)) return false;
+            if (OWN && !cl_wait(P, S.ofull + 8u * xw, pw)) return false;
+            if (SEND && wrapped && !cl_wait(P, S.empty + 8u * xo, pe)) return false;
+            const uint32_t in = S.inbox + xi * (uint32_t)kClStageBytes;
+            const uint32_t ow = S.own + xw * (uint32_t)kClStageBytes;
+            const uint32_t dst = dst_inbox + xo * (uint32_t)kClStageBytes;
+            const uint32_t dbar = dst_full + 8u * xo;
+            uint4* gout = mine + i0;
+            if (SEND) jitter_warp(P);
+            if (npk == TP) body<KIND, true>(in, ow, dst, dbar, gout, npk);
+            else body<KIND, false>(in, ow, dst, dbar, gout, npk);
+            __syncwarp();
+            if ((me & 31u) == 0) {
+                if (RECV) mbar_arrive_u32(S.cons + 8u * xi);   // my reads of the inbox stage are done
+                if (OWN) mbar_arrive_u32(S.oempty + 8u * xw);
+            }
+            if (RECV && ++xi == (uint32_t)kClStages) { xi = 0; pi ^= 1u; }
+            if (OWN && ++xw == (uint32_t)kClOwn) { xw = 0; pw ^= 1u; }
+            if (SEND && ++xo == (uint32_t)kClStages) { xo = 0; pe ^= 1u; wrapped = true; }
+        }
+        return true;
+    }
+};
+
+template <int DT, int OP>
+__global__ void __launch_bounds__(kClThreads, 1) ring_cluster_kernel(Params P) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int AW = AccWords<DT>::N;
+    constexpr int ES = DType<DT>::ES;
+    constexpr unsigned TP = cl_tile<AW>();
+    const int n = P.nranks;
+    const int r = (int)cluster_rank();
+    const int c = (int)blockIdx.x / n;
+    const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+    const bool tel = P.tel != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const unsigned long long tel_t0 = tel ? globaltimer() : 0;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ClRingSmem S = cl_ring_smem(smem_u32(smem));
+    const unsigned long long SP = cl_ring_sp<AW>(P);
+    unsigned long long ca, cb;
+    split_range(0, npacks<ES>(P), P.nch, c, ca, cb);
+    char* mine = P.bufs[r];
+    // bytes of a received tile: the predecessor sent AW words per pack before its
+    // final step (s - 1 < n - 1), one word after
+    auto recv_bytes = [&](const RingCursor& q) {
+        return ring_cursor_npk(q, TP) * 16u * (uint32_t)(q.s <= n - 1 ? AW : 1);
+    };
+    if (threadIdx.x == 0) {
+        for (int x = 0; x < kClStages; ++x) {
+            mbar_init_u32(S.full + 8u * x, 1);
+            mbar_init_u32(S.cons + 8u * x, kClWarps);
+            mbar_init_u32(S.empty + 8u * x, 1);
+        }
+        for (int x = 0; x < kClOwn; ++x) {
+            mbar_init_u32(S.ofull + 8u * x, 1);
+            mbar_init_u32(S.oempty + 8u * x, kClWarps);
+        }
+        mbar_init_u32(S.fin, (uint32_t)(n - 1));
+        mbar_fence_init();
+        // arm the first kClStages received tiles
+        RingCursor q = ring_cursor(r, n, ca, cb, SP);
+        for (int x = 0; x < kClStages; ++x) {
+            ring_cursor_recv(q, r, n, cb, SP, TP);
+            if (q.done) break;
+            mbar_expect_u32(S.full + 8u * x, recv_bytes(q));
+            ring_cursor_next(q, r, n, cb, SP, TP);
+        }
+    }
+    cluster_sync_all();   // every peer's barriers are initialised before any remote arrive / st.async
+
+    if (warp == 0) {
+        // ------------------------------------------------------------- loader
+        // own input tiles of the reduce-scatter steps (s <= n-1), in walk order.
+        // The whole warp walks (lane 0 issues): a lone lane looping while its
+        // warp-mates wait at the final __syncthreads diverges an aligned barrier
+        // (measured: the loader starves, 32 MiB takes 65 ms).
+        unsigned long long t = 0;
+        const bool ok = cl_ring_walk(r, n, ca, cb, SP, TP, [&](int s, unsigned long long i0, unsigned npk) {
+            if (s > n - 1) return true;
+            const uint32_t x = (uint32_t)(t % kClOwn);
+            if (t >= (unsigned long long)kClOwn &&
+                !__all_sync(0xffffffffu, cl_wait(P, S.oempty + 8u * x, (uint32_t)((t / kClOwn - 1) & 1))))
+                return false;
+            if (lane == 0) {
+                mbar_expect_u32(S.ofull + 8u * x, npk * 16u);
+                bulk_load_u32(S.own + x * (uint32_t)kClStageBytes, mine + i0 * 16ull, npk * 16u, S.ofull + 8u * x);
+            }
+            __syncwarp();
+            ++t;
+            return true;
+        });
+        if (!ok && lane == 0) {
+            // every bulk load issued must land before this CTA's shared memory goes away
+            const unsigned long long lo = t > (unsigned long long)kClOwn ? t - kClOwn : 0;
+            for (unsigned long long u = lo; u < t; ++u)
+                while (!cl_try_wait(S.ofull + 8u * (uint32_t)(u % kClOwn), (uint32_t)((u / kClOwn) & 1))) {}
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------------------- signal
+        // per received tile, once my compute warps have read its stage: re-arm the
+        // stage's `full` for the tile kClStages later, then return the credit
+        const uint32_t pred = (uint32_t)((r + n - 1) % n);
+        const uint32_t pred_empty = cl_map(S.empty, pred);
+        RingCursor ahead = ring_cursor(r, n, ca, cb, SP);
+        for (int x = 0; x < kClStages && !ahead.done; ++x) {
+            ring_cursor_recv(ahead, r, n, cb, SP, TP);
+            if (!ahead.done) ring_cursor_next(ahead, r, n, cb, SP, TP);
+        }
+        unsigned long long nr = 0;
+        for (RingCursor q = ring_cursor(r, n, ca, cb, SP);;) {
+            ring_cursor_recv(q, r, n, cb, SP, TP);
+            if (q.done) break;
+            const uint32_t x = (uint32_t)(nr % kClStages);
+            if (!__all_sync(0xffffffffu, cl_wait(P, S.cons + 8u * x, (uint32_t)((nr / kClStages) & 1)))) break;
+            ring_cursor_recv(ahead, r, n, cb, SP, TP);
+            if (lane == 0) {
+                if (!ahead.done) mbar_expect_u32(S.full + 8u * x, recv_bytes(ahead));
+                cl_arrive_remote(pred_empty + 8u * x);
+            }
+            __syncwarp();
+            if (!ahead.done) ring_cursor_next(ahead, r, n, cb, SP, TP);
+            ring_cursor_next(q, r, n, cb, SP, TP);
+            ++nr;
+        }
+    } else {
+        // ------------------------------------------------------- compute warps
+        const uint32_t succ = (uint32_t)((r + 1) % n);
+        ClCompute<DT, OP> cp;
+        cp.S = S;
+        cp.dst_inbox = cl_map(S.inbox, succ);
+        cp.dst_full = cl_map(S.full, succ);
+        cp.mine = reinterpret_cast<uint4*>(mine);
+        cp.me = (uint32_t)(warp - 2) * 32u + (uint32_t)lane;
+        const unsigned long long LC = SP * (unsigned long long)n;
+        bool ok = true;
+        for (unsigned long long base = ca; base < cb && ok; base += LC) {
+            const unsigned long long L = (cb - base < LC) ? cb - base : LC;
+            for (int s = 0; s < 2 * (n - 1) + 1 && ok; ++s) {
+                int k;
+                if (s < n) k = ((r - s) % n + n) % n;
+                else k = ((r - (s - n)) % n + n) % n;
+                if (s == n - 1) k = (r + 1) % n;
+                const unsigned long long ks = base + L * (unsigned long long)k / n;
+                const unsigned long long ke = base + L * (unsigned long long)(k + 1) / n;
+                // the step's kind is uniform: one specialised tile loop per kind
+                if (s == 0) ok = cp.template tiles<kClFirst>(P, ks, ke);
+                else if (s < n - 1) ok = cp.template tiles<kClMid>(P, ks, ke);
+                else if (s == n - 1) ok = cp.template tiles<kClFin>(P, ks, ke);
+                else if (s < 2 * (n - 1)) ok = cp.template tiles<kClAg>(P, ks, ke);
+                else ok = cp.template tiles<kClLast>(P, ks, ke);
+            }
+        }
+    }
+    cl_rendezvous(P, S.fin, r, n);
+    if (tel) {
+        volatile TelEntry* e = P.tel + (P.seq % kTelRing);
+        e->t0 = tel_t0;
+        e->t1 = globaltimer();
+        __threadfence_system();
+        e->seq = P.seq;
+    }
+}
+
+}  // namespace dev
+}  // namespace polar

@@ -158,6 +158,11 @@ struct polar_comm_s {
     // own transport (or POLAR_LL128_REAL=1 says so); virtual comms: one GPU,
     // probed by polar_probe_ll128 (profiles/r01_probe_ll128.jsonl)
     bool ll128_ok = true;
+    // virtual comms: ring / tree Simple as thread-block clusters (cluster.cuh;
+    // POLAR_CLUSTER=0 keeps the FIFO kernels); channel bound = clusters of n CTAs
+    // that fit on the GPU at once (cudaOccupancyMaxActiveClusters)
+    bool cluster = false;
+    int cl_max_ch[5] = {};               // per algorithm id
     std::mutex mu;
 };
 
@@ -290,6 +295,72 @@ polar_status launch_kernel(polar_comm_s* c, const void* fn, dev::Params& P, int 
     return POLAR_OK;
 }
 
+// Cluster-transport kernels (virtual comms): grid = nch clusters of n CTAs,
+// cluster rank = rank (cluster.cuh).  No cooperative attribute: a cluster's CTAs
+// are co-scheduled by the hardware and channels never wait on each other.
+polar_status launch_cluster(polar_comm_s* c, const void* fn, dev::Params& P, int algo, cudaStream_t stream) {
+    P.call = c->calls;
+    P.prev_tag = c->prev_tag;
+    void* args[] = {&P};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(P.nch * c->nranks));
+    cfg.blockDim = dim3((unsigned)cluster_threads());
+    cfg.dynamicSmemBytes = cluster_smem_bytes(algo);
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[2];
+    unsigned n = 0;
+    attrs[n].id = cudaLaunchAttributeClusterDimension;
+    attrs[n].val.clusterDim.x = (unsigned)c->nranks;
+    attrs[n].val.clusterDim.y = 1;
+    attrs[n].val.clusterDim.z = 1;
+    ++n;
+    if (c->pdl) {
+        attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = n;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess && c->pdl) {
+        (void)cudaGetLastError();
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelExC(&cfg, fn, args);
+    }
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return POLAR_ECUDA;
+    }
+    c->launches++;
+    c->calls++;
+    c->prev_tag = P.dtag;
+    return POLAR_OK;
+}
+
+// How many clusters of n CTAs of the algorithm's cluster kernel fit at once
+// (0: the cluster path is unavailable for it).
+int cluster_max_active(int algo, int nranks) {
+    const void* fn = cluster_kernel_for(POLAR_FLOAT32, POLAR_SUM, algo);
+    if (!fn) return 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nranks * POLAR_MAXCH));
+    cfg.blockDim = dim3((unsigned)cluster_threads());
+    cfg.dynamicSmemBytes = cluster_smem_bytes(algo);
+    cudaLaunchAttribute a{};
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = (unsigned)nranks;
+    a.val.clusterDim.y = 1;
+    a.val.clusterDim.z = 1;
+    cfg.attrs = &a;
+    cfg.numAttrs = 1;
+    int num = 0;
+    if (cudaOccupancyMaxActiveClusters(&num, fn, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return num;
+}
+
 polar_status init_barrier(polar_comm_s* c) {
     dev::Params P;
     fill_params(c, P);
@@ -342,6 +413,10 @@ polar_status alloc_common(polar_comm_s* c) {
             CU_TRY(cudaFuncSetAttribute(kernel_for(dt, op, POLAR_ALGO_RING, POLAR_PROTO_SIMPLE),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)dev::ring_tma_smem_bytes()));
+            for (int algo : {POLAR_ALGO_RING, POLAR_ALGO_TREE})
+                if (const void* fn = cluster_kernel_for(dt, op, algo))
+                    CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)cluster_smem_bytes(algo)));
         }
     c->timeout_ns = (unsigned long long)env_size("POLAR_TIMEOUT_MS", 20000) * 1000000ull;
     CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
@@ -622,7 +697,20 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         // closed loop: the row's nchannels is the cap, the controller picks c
         d.nchannels = c->ad.c < d.nchannels ? c->ad.c : d.nchannels;
     }
-    if (c->is_virtual) {
+    // virtual comms: ring / tree Simple on whole 16-B packs of 16-B aligned
+    // buffers run as clusters (cluster.cuh), bounded by the clusters that fit
+    bool use_cluster = false;
+    if (c->is_virtual && c->cluster && d.proto == POLAR_PROTO_SIMPLE &&
+        (d.algo == POLAR_ALGO_RING || d.algo == POLAR_ALGO_TREE) &&
+        c->cl_max_ch[d.algo] > 0 && (count * (size_t)es) % 16 == 0) {
+        use_cluster = true;
+        for (int p = 0; p < c->nranks && count > 0; ++p)
+            use_cluster = use_cluster && (reinterpret_cast<uintptr_t>(bufs[p]) % 16 == 0);
+        use_cluster = use_cluster && cluster_kernel_for(dtype, op, (int)d.algo) != nullptr;
+    }
+    if (use_cluster) {
+        if ((int)d.nchannels > c->cl_max_ch[d.algo]) d.nchannels = (uint32_t)c->cl_max_ch[d.algo];
+    } else if (c->is_virtual) {
         const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
     }
@@ -661,6 +749,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         }
         P.vec = vec;
         P.count = count;
+        if (use_cluster) return launch_cluster(c, cluster_kernel_for(dtype, op, (int)d.algo), P, (int)d.algo, stream);
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
     char* mine = reinterpret_cast<char*>(bufs[0]);
@@ -939,6 +1028,12 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
         }
         c->max_coop_blocks = sms * minper;
         if (st == POLAR_OK && c->max_coop_blocks < nranks) st = POLAR_EUNSUPPORTED;
+    }
+    if (st == POLAR_OK && nranks > 1) {
+        const char* ec = std::getenv("POLAR_CLUSTER");
+        c->cluster = !(ec && ec[0] == '0');
+        for (int algo : {POLAR_ALGO_RING, POLAR_ALGO_TREE})
+            c->cl_max_ch[algo] = c->cluster ? std::min(POLAR_MAXCH, cluster_max_active(algo, nranks)) : 0;
     }
     if (st == POLAR_OK) st = cuerr(cudaDeviceSynchronize());
     if (st == POLAR_OK) st = init_barrier(c);

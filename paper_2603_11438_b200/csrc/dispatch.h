@@ -1,6 +1,8 @@
 // Kernel table: one instantiation per <dtype, op, algorithm, protocol>, compiled
 // in inst_<dtype>.cu (one translation unit per dtype so nvcc runs in parallel).
 #pragma once
+#include <cstddef>
+
 #include "polar.h"
 
 namespace polar {
@@ -20,6 +22,12 @@ const void* direct_kernel_bf16(int mode, int op);
 // NVLS (switch reduction, nvls.cu): nullptr where the switch has no such
 // reduction (f32 min / max)
 const void* nvls_kernel_for(int dtype, int op);
+
+// Cluster-transport ring / tree Simple for virtual comms (cluster.cu): nullptr
+// where no cluster kernel exists; its dynamic shared memory and block size
+const void* cluster_kernel_for(int dtype, int op, int algo);
+size_t cluster_smem_bytes(int algo);
+int cluster_threads();
 
 inline const void* direct_kernel_for(int dtype, int mode, int op) {
     switch (dtype) {
