@@ -452,6 +452,10 @@ def run_polar(args):
     else:
         sweep = c2_sweep_virtual(L, comm, big, n, stream, t_step)
     comm.check()
+    # virtual N=1: every algorithm's Simple kernel at the C2 size against the
+    # same HBM roofline (ring / tree on both transports: clusters, and the
+    # peer-memory FIFOs that real comms run)
+    algos = None if real else algorithm_records(L, big, n, stream, peak_for_records())
 
     # e2e: through the C-ABI with HOST buffers; H2D + allreduce + D2H inside the timed region
     host = [torch.from_numpy(x).pin_memory() for x in host_inputs]
@@ -529,6 +533,8 @@ def run_polar(args):
             "clocks": clocks.summary(), ("nvlink_sweep" if real else "c2_sweep"): sweep,
             "decision_cost_ns": decision_cost(L), "p2p_probe": probe_out,
         }
+        if algos is not None:
+            out["algorithms"] = algos
         if ll128_probe is not None:
             out["ll128_probe"] = ll128_probe
         if unreg is not None:
@@ -609,6 +615,60 @@ def _time_calls(fn, iters, stream, flush=None):
     for a, b in evs:
         tot += a.elapsed_time(b) / 1e3
     return tot / iters
+
+
+def peak_for_records():
+    return load_peaks()[0]
+
+
+def algorithm_records(L, big, n, stream, peak):
+    """Each algorithm's Simple kernel, forced, on the bench's own buffers at the
+    C2 size (8 virtual ranks x 128 MiB, f32 and bf16), back to back: us, busBW
+    and the fraction of the HBM copy peak its algorithmic bytes (2 n S: every
+    input read once, every output written once) reach.  Ring and tree run on
+    both virtual transports: "cluster" (one thread-block cluster per channel,
+    DSMEM hops; the default) and "peer" (the FIFO kernels through global
+    memory, POLAR_CLUSTER=0), whatever the size."""
+    import torch
+    out = {}
+    comms = {}
+    old = os.environ.get("POLAR_CLUSTER")
+    for tr, env in (("cluster", "1"), ("peer", "0")):
+        os.environ["POLAR_CLUSTER"] = env
+        os.environ["POLAR_CLUSTER_TREE_MAX"] = str(1 << 40) if tr == "cluster" else str(16 << 20)
+        comms[tr] = L.Comm.virtual(n, torch.cuda.current_device())
+    if old is None:
+        os.environ.pop("POLAR_CLUSTER", None)
+    else:
+        os.environ["POLAR_CLUSTER"] = old
+    os.environ.pop("POLAR_CLUSTER_TREE_MAX", None)
+    sptr = stream.cuda_stream
+    ptrs = [b.data_ptr() for b in big]
+    try:
+        for dt, code, es in (("f32", L.FLOAT32, 4), ("bf16", L.BFLOAT16, 2)):
+            cnt = S_BYTES // es
+            for algo, tr in (("twoshot", "peer"), ("ring", "cluster"), ("ring", "peer"),
+                             ("tree", "cluster"), ("tree", "peer")):
+                c = comms[tr]
+                dec = L.Decision(L.ALGO_CODES[algo], L.SIMPLE, 32, 0)
+
+                def call():
+                    st = c.allreduce_forced_raw(ptrs, cnt, code, L.SUM, dec, sptr)
+                    if st != 0:
+                        raise L.PolarError(st, "polar_allreduce_forced")
+                for _ in range(3):
+                    call()
+                torch.cuda.synchronize()
+                t = _time_calls(call, 10, stream)
+                c.check()
+                out[f"{algo}/{tr}/{dt}"] = {
+                    "us": round(t * 1e6, 1), "busbw_gbs": round(busbw(S_BYTES, n, t), 1),
+                    "hbm_frac": round(2 * n * S_BYTES / t / 1e9 / peak, 4),
+                    "transport": c.transport(), "launched_channels": c.launched_channels()}
+    finally:
+        for c in comms.values():
+            c.destroy()
+    return out
 
 
 def c2_sweep_virtual(L, comm, big, n, stream, t_step):

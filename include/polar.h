@@ -362,6 +362,19 @@ polar_status polar_comm_last_decision(polar_comm_t comm, polar_decision* out);
  * (nchannels x nlocal).  Either pointer may be NULL. */
 polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint32_t* grid);
 
+/* Transport of the most recent AllReduce on this comm: POLAR_TRANSPORT_PEER
+ * (kernels exchange through peer-mapped / global memory: every real comm, and
+ * virtual comms for one-shot, two-shot, LL / LL128 and unaligned buffers) or
+ * POLAR_TRANSPORT_CLUSTER (virtual comms, ring / tree Simple on whole 16-B packs
+ * of 16-B aligned buffers: the n ranks of a channel are the n CTAs of one
+ * thread-block cluster and every hop is a distributed-shared-memory store;
+ * DESIGN.md §8 "Cluster transport").  Same algorithm, schedule and reduction
+ * order either way.  POLAR_CLUSTER=0 (read at polar_comm_init_virtual) keeps
+ * virtual comms on the peer transport; POLAR_CLUSTER_TREE_MAX (bytes per rank,
+ * default 16 MiB) bounds the sizes that run the cluster tree. */
+enum { POLAR_TRANSPORT_PEER = 0, POLAR_TRANSPORT_CLUSTER = 1 };
+polar_status polar_comm_transport(polar_comm_t comm, int* transport);
+
 /* Number of kernels this comm has launched so far (evidence for bench.py). */
 uint64_t polar_comm_launches(polar_comm_t comm);
 

@@ -44,6 +44,9 @@ namespace dev {
 #ifndef POLAR_CL_STAGES
 #define POLAR_CL_STAGES 10        // ring inbox stages (>= tiles per ring step + slack)
 #endif
+#ifndef POLAR_CL_MINB
+#define POLAR_CL_MINB 1           // CTAs per SM the register budget is sized for
+#endif
 #ifndef POLAR_CL_PROF
 #define POLAR_CL_PROF 0           // diagnostic wait-time counters into P.trace
 #endif
@@ -417,7 +420,7 @@ struct ClCompute {
 };
 
 template <int DT, int OP>
-__global__ void __launch_bounds__(kClThreads, 1) ring_cluster_kernel(Params P) {
+__global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel(Params P) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr int AW = AccWords<DT>::N;
@@ -545,6 +548,263 @@ __global__ void __launch_bounds__(kClThreads, 1) ring_cluster_kernel(Params P) {
                 else if (s < 2 * (n - 1)) ok = cp.template tiles<kClAg>(P, ks, ke);
                 else ok = cp.template tiles<kClLast>(P, ks, ke);
             }
+        }
+    }
+    cl_rendezvous(P, S.fin, r, n);
+    if (tel) {
+        volatile TelEntry* e = P.tel + (P.seq % kTelRing);
+        e->t0 = tel_t0;
+        e->t1 = globaltimer();
+        __threadfence_system();
+        e->seq = P.seq;
+    }
+}
+
+// ======================================================================= tree
+// Binary tree Simple over a cluster (the FIFO tree's topology and reduction
+// order: positions pos = (rank - c) mod n, root = rank c mod n, children
+// 2pos+1, 2pos+2; node = own (op) child0 (op) child1, bf16 partials in f32).
+// Every hop is an st.async into the receiver's shared-memory inbox; the tree
+// is acyclic, so a few stages per link cover the credit round trip.
+//   warp 0      loader: own input tiles (TMA) into kTrOwn stages
+//   warps 1-4   up group: own (op) children -> parent's up inbox (AW words);
+//               the root rounds once, stores, and sends the result down
+//   warps 5-8   down group (non-root): parent's result -> HBM + children
+// Full barriers are armed by the senders' warps (remote arrive.expect_tx with
+// the bytes each warp sent), credits are returned by each consuming warp: the
+// up and down groups have kTrGroup warps each, so every count is kTrGroup.
+#ifndef POLAR_TR_WIRE
+#define POLAR_TR_WIRE 1024        // 16-B wire words per stage (16 KiB)
+#endif
+#ifndef POLAR_TR_UP
+#define POLAR_TR_UP 4             // stages per child up inbox
+#endif
+#ifndef POLAR_TR_DN
+#define POLAR_TR_DN 3             // stages of the down inbox
+#endif
+#ifndef POLAR_TR_OWN
+#define POLAR_TR_OWN 2            // own-input stages
+#endif
+#ifndef POLAR_TR_GROUP
+#define POLAR_TR_GROUP 4          // warps per group (up, down)
+#endif
+constexpr unsigned kTrWire = POLAR_TR_WIRE;
+constexpr size_t kTrStage = (size_t)kTrWire * 16;
+constexpr int kTrUp = POLAR_TR_UP, kTrDn = POLAR_TR_DN, kTrOwn = POLAR_TR_OWN, kTrGroup = POLAR_TR_GROUP;
+constexpr int kTrThreads = 32 * (1 + 2 * kTrGroup);
+constexpr int kTrNbar = 2 * kTrUp + kTrUp + kTrDn + 2 * kTrDn + 2 * kTrOwn + 1;
+__host__ __device__ constexpr size_t cl_tree_smem_bytes() {
+    return (size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8;
+}
+struct ClTreeSmem {
+    uint32_t up[2], dn, own;            // inboxes (child k up, parent down), own stages
+    uint32_t upfull[2], upempty;        // up inbox k landed / my up sends' credits
+    uint32_t dnfull, dnempty[2];        // down inbox landed / my down sends to child k: credits
+    uint32_t ofull, oempty, fin;
+};
+__device__ __forceinline__ ClTreeSmem cl_tree_smem(uint32_t base) {
+    ClTreeSmem t;
+    uint32_t o = base;
+    t.up[0] = o; o += (uint32_t)(kTrUp * kTrStage);
+    t.up[1] = o; o += (uint32_t)(kTrUp * kTrStage);
+    t.dn = o; o += (uint32_t)(kTrDn * kTrStage);
+    t.own = o; o += (uint32_t)(kTrOwn * kTrStage);
+    t.upfull[0] = o; o += 8u * kTrUp;
+    t.upfull[1] = o; o += 8u * kTrUp;
+    t.upempty = o; o += 8u * kTrUp;
+    t.dnfull = o; o += 8u * kTrDn;
+    t.dnempty[0] = o; o += 8u * kTrDn;
+    t.dnempty[1] = o; o += 8u * kTrDn;
+    t.ofull = o; o += 8u * kTrOwn;
+    t.oempty = o; o += 8u * kTrOwn;
+    t.fin = o;
+    return t;
+}
+// a ring counter: stage index and the parity of the phase to wait for
+struct StageCtr {
+    uint32_t x = 0, par = 0;
+    bool wrapped = false;
+    __device__ __forceinline__ void next(uint32_t D) {
+        if (++x == D) { x = 0; par ^= 1u; wrapped = true; }
+    }
+};
+
+template <int DT, int OP>
+__global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int AW = AccWords<DT>::N;
+    constexpr int ES = DType<DT>::ES;
+    constexpr unsigned TP = kTrWire / (unsigned)AW;            // element packs per tile
+    constexpr unsigned NT = kTrGroup * 32;
+    constexpr unsigned PPL = (TP + NT - 1) / NT;
+    const int n = P.nranks;
+    const int r = (int)cluster_rank();
+    const int c = (int)blockIdx.x / n;
+    const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+    const int pos = ((r - c) % n + n) % n;
+    auto rank_of = [&](int q) { return (q + c) % n; };
+    const bool root = pos == 0;
+    const int parent = root ? -1 : rank_of((pos - 1) / 2);
+    const int my_idx = root ? 0 : (pos - 1) % 2;
+    int child[2] = {-1, -1};
+    int nchild = 0;
+    for (int k = 0; k < 2; ++k)
+        if (2 * pos + 1 + k < n) { child[k] = rank_of(2 * pos + 1 + k); nchild = k + 1; }
+    const bool tel = P.tel != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const unsigned long long tel_t0 = tel ? globaltimer() : 0;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ClTreeSmem S = cl_tree_smem(smem_u32(smem));
+    if (threadIdx.x == 0) {
+        for (int x = 0; x < kTrUp; ++x) {
+            mbar_init_u32(S.upfull[0] + 8u * x, kTrGroup);
+            mbar_init_u32(S.upfull[1] + 8u * x, kTrGroup);
+            mbar_init_u32(S.upempty + 8u * x, kTrGroup);
+        }
+        for (int x = 0; x < kTrDn; ++x) {
+            mbar_init_u32(S.dnfull + 8u * x, kTrGroup);
+            mbar_init_u32(S.dnempty[0] + 8u * x, kTrGroup);
+            mbar_init_u32(S.dnempty[1] + 8u * x, kTrGroup);
+        }
+        for (int x = 0; x < kTrOwn; ++x) {
+            mbar_init_u32(S.ofull + 8u * x, 1);
+            mbar_init_u32(S.oempty + 8u * x, kTrGroup);
+        }
+        mbar_init_u32(S.fin, (uint32_t)(n - 1));
+        mbar_fence_init();
+    }
+    cluster_sync_all();
+    unsigned long long ca, cb;
+    split_range(0, npacks<ES>(P), P.nch, c, ca, cb);
+    uint4* mine = reinterpret_cast<uint4*>(P.bufs[r]);
+    // remote addresses: my up inbox slot at the parent, the children's down inboxes
+    const uint32_t par_up = root ? 0u : cl_map(S.up[my_idx], (uint32_t)parent);
+    const uint32_t par_upfull = root ? 0u : cl_map(S.upfull[my_idx], (uint32_t)parent);
+    const uint32_t par_dnempty = root ? 0u : cl_map(S.dnempty[my_idx], (uint32_t)parent);
+    uint32_t ch_dn[2] = {0, 0}, ch_dnfull[2] = {0, 0}, ch_upempty[2] = {0, 0};
+    for (int k = 0; k < nchild; ++k) {
+        ch_dn[k] = cl_map(S.dn, (uint32_t)child[k]);
+        ch_dnfull[k] = cl_map(S.dnfull, (uint32_t)child[k]);
+        ch_upempty[k] = cl_map(S.upempty, (uint32_t)child[k]);
+    }
+    // the bytes a warp of a group sends for its packs of a tile of npk packs
+    auto warp_packs = [&](int gw, unsigned npk) {
+        uint32_t cnt = 0;
+#pragma unroll
+        for (unsigned u = 0; u < PPL; ++u) {
+            const unsigned b0 = u * NT + (unsigned)gw * 32;
+            cnt += npk > b0 ? (npk - b0 < 32 ? npk - b0 : 32) : 0;
+        }
+        return cnt;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------- loader
+        StageCtr w;
+        bool ok = true;
+        unsigned long long issued = 0;
+        for (unsigned long long i0 = ca; i0 < cb && ok; i0 += TP) {
+            const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
+            if (w.wrapped && !__all_sync(0xffffffffu, cl_wait(P, S.oempty + 8u * w.x, w.par ^ 1u))) { ok = false; break; }
+            if (lane == 0) {
+                mbar_expect_u32(S.ofull + 8u * w.x, npk * 16u);
+                bulk_load_u32(S.own + w.x * (uint32_t)kTrStage, mine + i0, npk * 16u, S.ofull + 8u * w.x);
+            }
+            __syncwarp();
+            ++issued;
+            w.next(kTrOwn);
+        }
+        if (!ok && lane == 0) {
+            const unsigned long long lo = issued > (unsigned long long)kTrOwn ? issued - kTrOwn : 0;
+            for (unsigned long long u = lo; u < issued; ++u)
+                while (!cl_try_wait(S.ofull + 8u * (uint32_t)(u % kTrOwn), (uint32_t)((u / kTrOwn) & 1))) {}
+        }
+        __syncwarp();
+    } else if (warp <= kTrGroup) {
+        // ----------------------------------------------------------- up group
+        const int gw = warp - 1;
+        const unsigned me = (unsigned)gw * 32u + (unsigned)lane;
+        StageCtr w, in, up, dn;   // own stage, child up inboxes (both children in step), my up sends, my down sends
+        for (unsigned long long i0 = ca; i0 < cb; i0 += TP) {
+            const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
+            if (!cl_wait(P, S.ofull + 8u * w.x, w.par)) break;
+            bool ok = true;
+            for (int k = 0; k < nchild; ++k) ok = ok && cl_wait(P, S.upfull[k] + 8u * in.x, in.par);
+            if (!root && up.wrapped) ok = ok && cl_wait(P, S.upempty + 8u * up.x, up.par ^ 1u);
+            if (root)
+                for (int k = 0; k < nchild; ++k)
+                    if (dn.wrapped) ok = ok && cl_wait(P, S.dnempty[k] + 8u * dn.x, dn.par ^ 1u);
+            if (!ok) break;
+            const uint32_t ow = S.own + w.x * (uint32_t)kTrStage;
+            const uint32_t cin0 = S.up[0] + in.x * (uint32_t)kTrStage, cin1 = S.up[1] + in.x * (uint32_t)kTrStage;
+            const uint32_t dst = par_up + up.x * (uint32_t)kTrStage, dbar = par_upfull + 8u * up.x;
+            if (!root || nchild) jitter_warp(P);
+#pragma unroll
+            for (unsigned u = 0; u < PPL; ++u) {
+                const unsigned p = u * NT + me;
+                if (p >= npk) break;
+                Acc<DT> acc;
+                acc_init<DT>(acc, ld_shared_v4(ow + p * 16u));
+                for (int k = 0; k < nchild; ++k) {
+                    Acc<DT> chv;
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) chv.w[q] = ld_shared_v4((k ? cin1 : cin0) + ((unsigned)q * TP + p) * 16u);
+                    acc_merge<DT, OP>(acc, chv);
+                }
+                if (root) {
+                    const uint4 v = acc_fin<DT>(acc);
+                    st_plain(mine + i0 + p, v);
+                    for (int k = 0; k < nchild; ++k) cl_st_async(ch_dn[k] + dn.x * (uint32_t)kTrStage + p * 16u, v,
+                                                                 ch_dnfull[k] + 8u * dn.x);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < AW; ++q) cl_st_async(dst + ((unsigned)q * TP + p) * 16u, acc.w[q], dbar);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t cnt = warp_packs(gw, npk);
+                mbar_arrive_u32(S.oempty + 8u * w.x);
+                for (int k = 0; k < nchild; ++k) cl_arrive_remote(ch_upempty[k] + 8u * in.x);   // credits to children
+                if (!root) cl_arrive_expect_remote(dbar, cnt * 16u * (uint32_t)AW);
+                else
+                    for (int k = 0; k < nchild; ++k) cl_arrive_expect_remote(ch_dnfull[k] + 8u * dn.x, cnt * 16u);
+            }
+            w.next(kTrOwn);
+            if (nchild) in.next(kTrUp);
+            if (!root) up.next(kTrUp);
+            else if (nchild) dn.next(kTrDn);
+        }
+    } else if (!root) {
+        // --------------------------------------------------------- down group
+        const int gw = warp - 1 - kTrGroup;
+        const unsigned me = (unsigned)gw * 32u + (unsigned)lane;
+        StageCtr in, dn;
+        for (unsigned long long i0 = ca; i0 < cb; i0 += TP) {
+            const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
+            bool ok = cl_wait(P, S.dnfull + 8u * in.x, in.par);
+            for (int k = 0; k < nchild; ++k)
+                if (dn.wrapped) ok = ok && cl_wait(P, S.dnempty[k] + 8u * dn.x, dn.par ^ 1u);
+            if (!ok) break;
+            const uint32_t src = S.dn + in.x * (uint32_t)kTrStage;
+            if (nchild) jitter_warp(P);
+#pragma unroll
+            for (unsigned u = 0; u < PPL; ++u) {   // down tiles: TP packs of one word
+                const unsigned p = u * NT + me;
+                if (p >= npk) break;
+                const uint4 v = ld_shared_v4(src + p * 16u);
+                st_plain(mine + i0 + p, v);
+                for (int k = 0; k < nchild; ++k) cl_st_async(ch_dn[k] + dn.x * (uint32_t)kTrStage + p * 16u, v,
+                                                             ch_dnfull[k] + 8u * dn.x);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t cnt = warp_packs(gw, npk);
+                cl_arrive_remote(par_dnempty + 8u * in.x);   // credit to the parent
+                for (int k = 0; k < nchild; ++k) cl_arrive_expect_remote(ch_dnfull[k] + 8u * dn.x, cnt * 16u);
+            }
+            in.next(kTrDn);
+            if (nchild) dn.next(kTrDn);
         }
     }
     cl_rendezvous(P, S.fin, r, n);

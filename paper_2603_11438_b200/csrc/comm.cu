@@ -121,6 +121,7 @@ struct polar_comm_s {
     int* err_dev = nullptr;
     polar_decision last{};
     uint32_t last_nch = 0;
+    int last_transport = POLAR_TRANSPORT_PEER;
     uint64_t launches = 0;
     uint64_t calls = 0;                  // collective launches on this comm (identical on every rank)
     uint64_t prev_tag = 0;               // decision tag of the previous launch
@@ -163,6 +164,7 @@ struct polar_comm_s {
     // that fit on the GPU at once (cudaOccupancyMaxActiveClusters)
     bool cluster = false;
     int cl_max_ch[5] = {};               // per algorithm id
+    size_t cl_tree_max = 16u << 20;      // cluster tree up to this many bytes per rank (POLAR_CLUSTER_TREE_MAX)
     std::mutex mu;
 };
 
@@ -304,7 +306,7 @@ polar_status launch_cluster(polar_comm_s* c, const void* fn, dev::Params& P, int
     void* args[] = {&P};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(P.nch * c->nranks));
-    cfg.blockDim = dim3((unsigned)cluster_threads());
+    cfg.blockDim = dim3((unsigned)cluster_threads(algo));
     cfg.dynamicSmemBytes = cluster_smem_bytes(algo);
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
@@ -344,7 +346,7 @@ int cluster_max_active(int algo, int nranks) {
     if (!fn) return 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(nranks * POLAR_MAXCH));
-    cfg.blockDim = dim3((unsigned)cluster_threads());
+    cfg.blockDim = dim3((unsigned)cluster_threads(algo));
     cfg.dynamicSmemBytes = cluster_smem_bytes(algo);
     cudaLaunchAttribute a{};
     a.id = cudaLaunchAttributeClusterDimension;
@@ -702,7 +704,8 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     bool use_cluster = false;
     if (c->is_virtual && c->cluster && d.proto == POLAR_PROTO_SIMPLE &&
         (d.algo == POLAR_ALGO_RING || d.algo == POLAR_ALGO_TREE) &&
-        c->cl_max_ch[d.algo] > 0 && (count * (size_t)es) % 16 == 0) {
+        c->cl_max_ch[d.algo] > 0 && (count * (size_t)es) % 16 == 0 &&
+        (d.algo == POLAR_ALGO_RING || count * (size_t)es <= c->cl_tree_max)) {
         use_cluster = true;
         for (int p = 0; p < c->nranks && count > 0; ++p)
             use_cluster = use_cluster && (reinterpret_cast<uintptr_t>(bufs[p]) % 16 == 0);
@@ -715,6 +718,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
     }
     c->last_nch = d.nchannels;        // what is launched
+    c->last_transport = use_cluster ? POLAR_TRANSPORT_CLUSTER : POLAR_TRANSPORT_PEER;
     if (count == 0 || c->nranks == 1) return POLAR_OK;
     DeviceGuard dg(c->device);
     if (!dg.ok) return POLAR_ECUDA;
@@ -871,6 +875,7 @@ polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* cons
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;
     }
     c->last_nch = d.nchannels;
+    c->last_transport = POLAR_TRANSPORT_PEER;
     if (count == 0) return POLAR_OK;
     DeviceGuard dg(c->device);
     if (!dg.ok) return POLAR_ECUDA;
@@ -1032,6 +1037,11 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
     if (st == POLAR_OK && nranks > 1) {
         const char* ec = std::getenv("POLAR_CLUSTER");
         c->cluster = !(ec && ec[0] == '0');
+        // The cluster tree's interior nodes carry 3 S of DSMEM traffic each way
+        // (up: 2 children in, 1 out; down: 1 in, 2 out) through one SM's port:
+        // faster than the FIFO tree up to 16-32 MiB per rank, slower above
+        // (DESIGN.md §8 "Cluster transport"; profiles/r02aa_cluster_tree_ab.jsonl)
+        c->cl_tree_max = env_size("POLAR_CLUSTER_TREE_MAX", 16u << 20);
         for (int algo : {POLAR_ALGO_RING, POLAR_ALGO_TREE})
             c->cl_max_ch[algo] = c->cluster ? std::min(POLAR_MAXCH, cluster_max_active(algo, nranks)) : 0;
     }
@@ -1330,6 +1340,12 @@ polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint
     if (!comm) return POLAR_EINVAL;
     if (nchannels) *nchannels = comm->last_nch;
     if (grid) *grid = comm->last_nch * (uint32_t)comm->nlocal;
+    return POLAR_OK;
+}
+
+polar_status polar_comm_transport(polar_comm_t comm, int* transport) {
+    if (!comm || !transport) return POLAR_EINVAL;
+    *transport = comm->last_transport;
     return POLAR_OK;
 }
 

@@ -27,7 +27,7 @@ const void* nvls_kernel_for(int dtype, int op);
 // where no cluster kernel exists; its dynamic shared memory and block size
 const void* cluster_kernel_for(int dtype, int op, int algo);
 size_t cluster_smem_bytes(int algo);
-int cluster_threads();
+int cluster_threads(int algo);
 
 inline const void* direct_kernel_for(int dtype, int mode, int op) {
     switch (dtype) {

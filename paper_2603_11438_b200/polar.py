@@ -37,6 +37,7 @@ ALGO_CODES = {"tree": TREE, "ring": RING, "nvls": NVLS, "oneshot": ONESHOT, "two
 PROTO_CODES = {"ll": LL, "ll128": LL128, "simple": SIMPLE}
 ALGO_NAMES = {v: k for k, v in ALGO_CODES.items()}
 PROTO_NAMES = {v: k for k, v in PROTO_CODES.items()}
+TRANSPORT_NAMES = {0: "peer", 1: "cluster"}
 
 
 class PolarError(RuntimeError):
@@ -126,6 +127,7 @@ _sigs = {
     "polar_comm_last_decision": (C.c_int, [_P, C.POINTER(Decision)]),
     "polar_comm_launches": (C.c_uint64, [_P]),
     "polar_comm_launch_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "polar_comm_transport": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "polar_comm_check": (C.c_int, [_P]),
     "polar_comm_set_trace": (C.c_int, [_P, _P, C.c_size_t]),
     "polar_p2p_probe": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, _P]),
@@ -396,6 +398,12 @@ class Comm:
         _check(lib.polar_allreduce_forced(self.h, arr, n, dt, OP_CODES[op], C.byref(d), _stream_ptr(stream)),
                "polar_allreduce_forced")
 
+    def allreduce_forced_raw(self, ptrs, count, dtype_code, op_code, decision, stream_ptr):
+        """polar_allreduce_forced on raw device pointers (bench loops); returns the status."""
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        return lib.polar_allreduce_forced(self.h, arr, count, dtype_code, op_code, C.byref(decision),
+                                          C.c_void_p(stream_ptr))
+
     def _ptrs(self, tensors, what):
         tensors = self._list(tensors, what)
         return (C.c_void_p * self.nlocal)(*[t.data_ptr() for t in tensors]), tensors[0]
@@ -475,6 +483,12 @@ class Comm:
         nch = C.c_uint32(0)
         _check(lib.polar_comm_launch_info(self.h, C.byref(nch), None), "polar_comm_launch_info")
         return nch.value
+
+    def transport(self) -> str:
+        """Transport of the most recent AllReduce: "peer" or "cluster" (polar.h)."""
+        t = C.c_int(0)
+        _check(lib.polar_comm_transport(self.h, C.byref(t)), "polar_comm_transport")
+        return TRANSPORT_NAMES[t.value]
 
     def launches(self) -> int:
         return lib.polar_comm_launches(self.h)

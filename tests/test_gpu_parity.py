@@ -127,14 +127,16 @@ def test_back_to_back_alternating_no_sync():
 
 
 @pytest.mark.parametrize("algo", ["tree", "ring"])
-def test_simple_fifo_unit_sizes_back_to_back(algo):
+def test_simple_fifo_unit_sizes_back_to_back(algo, monkeypatch):
     """Warp-specialised ring/tree Simple (kernels.cuh ring_simple_ws /
     tree_simple_ws): back-to-back calls whose channels hold 1 tiny slot, a few
     slots (tree: half-slot units) and many slots (tree: whole-slot units) on one
     stream without host sync, mixed with LL calls that advance the same FIFO
-    counters: the half-slot tail encoding must keep every wait exact."""
+    counters: the half-slot tail encoding must keep every wait exact.  On a
+    POLAR_CLUSTER=0 comm: the FIFO kernels for every size."""
     n, dtype = 8, "f32"
-    c = comm(n)
+    monkeypatch.setenv("POLAR_CLUSTER", "0")
+    c = L.Comm.virtual(n, 0)
     plan = [(1000, "simple", 4), ((1 << 20) // 4, "simple", 18), ((24 << 20) // 4, "simple", 18),
             (777, "ll", 4), ((3 << 20) // 4 + 5, "simple", 8), (5, "simple", 2), ((40 << 20) // 4, "simple", 32),
             ((1 << 20) // 4, "ll128", 18), ((2 << 20) // 4, "simple", 18)]
@@ -148,6 +150,7 @@ def test_simple_fifo_unit_sizes_back_to_back(algo):
     c.check()
     for xs, ts in pending:
         check_result([to_host(t, dtype) for t in ts], xs, dtype, "sum", algo, n)
+    c.destroy()
 
 
 def test_policy_selected_decision_matches_oracle():
@@ -410,6 +413,7 @@ def test_ring_tma_forced(flags, monkeypatch):
     L2 eviction hints, bit 1 discard of consumed FIFO lines."""
     monkeypatch.setenv("POLAR_RING_TMA", "1")
     monkeypatch.setenv("POLAR_RING_TMA_FLAGS", flags)
+    monkeypatch.setenv("POLAR_CLUSTER", "0")   # the FIFO kernels (aligned sizes would run as clusters)
     for n in (2, 3, 8):
         c = L.Comm.virtual(n, 0)
         try:
