@@ -38,11 +38,35 @@
 namespace polar {
 namespace dev {
 
+// POLAR_CL_AGL2=1: the ring's all-gather through L2 instead of DSMEM (pull
+// from the predecessor's buffer with TMA; DESIGN.md §8 "Cluster transport",
+// measured variant).  Correct (the cluster GPU tests pass with it) but slower
+// on 8 x 128 MiB: f32 739 vs 685 us, bf16 1413 vs 926 us — two pull stages of
+// shared memory hold too few bytes in flight for the L2 round trip, and the
+// reduce-scatter inbox needs the rest of the 227 KB.  Off by default.
+#ifndef POLAR_CL_AGL2
+#define POLAR_CL_AGL2 0
+#endif
 #ifndef POLAR_CL_WARPS
-#define POLAR_CL_WARPS 8          // compute warps (warp 0 loads, warp 1 signals)
+#define POLAR_CL_WARPS 8          // compute warps (warp 0 loads, warp 1 signals, [last: all-gather])
 #endif
 #ifndef POLAR_CL_STAGES
-#define POLAR_CL_STAGES 10        // ring inbox stages (>= tiles per ring step + slack)
+#if POLAR_CL_AGL2
+#define POLAR_CL_STAGES 8         // ring inbox stages (>= tiles per ring step + slack)
+#define POLAR_CL_SLACK 2
+#else
+#define POLAR_CL_STAGES 10
+#define POLAR_CL_SLACK 4
+#endif
+#endif
+#ifndef POLAR_CL_AGP
+#define POLAR_CL_AGP 2            // all-gather pull stages (POLAR_CL_AGL2)
+#endif
+#ifndef POLAR_CL_AGF
+#define POLAR_CL_AGF 2            // final-tile stages (POLAR_CL_AGL2)
+#endif
+#ifndef POLAR_CL_AGLAG
+#define POLAR_CL_AGLAG 1          // pull stores in flight before a tile is published
 #endif
 #ifndef POLAR_CL_MINB
 #define POLAR_CL_MINB 1           // CTAs per SM the register budget is sized for
@@ -51,10 +75,19 @@ namespace dev {
 #define POLAR_CL_PROF 0           // diagnostic wait-time counters into P.trace
 #endif
 #ifndef POLAR_CL_OWN
-#define POLAR_CL_OWN 3            // own-input stages (TMA loads in flight)
+#if POLAR_CL_AGL2
+#define POLAR_CL_OWN 2            // own-input stages (TMA loads in flight)
+#else
+#define POLAR_CL_OWN 3
+#endif
 #endif
 constexpr int kClWarps = POLAR_CL_WARPS;
-constexpr int kClThreads = 32 * (kClWarps + 2);
+constexpr bool kClAgL2 = POLAR_CL_AGL2 != 0;
+constexpr int kClAgP = kClAgL2 ? POLAR_CL_AGP : 0;
+constexpr int kClAgF = kClAgL2 ? POLAR_CL_AGF : 0;
+constexpr int kClAg = kClAgP + kClAgF;
+constexpr int kClAgLag = POLAR_CL_AGLAG;
+constexpr int kClThreads = 32 * (kClWarps + 2 + (kClAgL2 ? 2 : 0));
 constexpr int kClStages = POLAR_CL_STAGES;
 constexpr int kClOwn = POLAR_CL_OWN;
 #ifndef POLAR_CL_WIRE
@@ -65,9 +98,10 @@ constexpr size_t kClStageBytes = (size_t)kClWire * 16;
 // element packs per tile: a tile's wire words fill one stage (bf16: 2 f32 words per pack)
 template <int AW> __host__ __device__ constexpr unsigned cl_tile() { return kClWire / (unsigned)AW; }
 // ring inbox stages needed per ring step + slack for the credit round trip
-constexpr int kClSlack = 4;
+constexpr int kClSlack = POLAR_CL_SLACK;
 __host__ __device__ constexpr size_t cl_ring_smem_bytes() {
-    return (size_t)(kClStages + kClOwn) * kClStageBytes + (size_t)(3 * kClStages + 2 * kClOwn + 1) * 8;
+    return (size_t)(kClStages + kClOwn + kClAg) * kClStageBytes +
+           (size_t)(3 * kClStages + 2 * kClOwn + kClAg + 3) * 8;
 }
 
 // ----------------------------------------------------------- cluster primitives
@@ -181,6 +215,29 @@ __device__ __forceinline__ bool cl_wait(const Params& P, uint32_t bar, uint32_t 
     if (cl_try_wait(bar, parity)) return true;
     return cl_wait_slow(bar, parity, P.timeout_ns, P.err, 1);
 }
+// Bounded wait until the u32 at shared address `a` (a monotone count) is >= v.
+static __device__ __noinline__ bool cl_wait_count_slow(uint32_t a, uint32_t v, unsigned long long timeout_ns, int* err) {
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1;; ++it) {
+        uint32_t c;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(c) : "r"(a) : "memory");
+        if (c >= v) return true;
+        if ((it & 63) == 0) {
+            if (globaltimer() - t0 > timeout_ns) {
+                *(volatile int*)err = POLAR_ETIMEOUT;
+                __threadfence_system();
+                return false;
+            }
+            if (*(volatile int*)err) return false;
+        }
+    }
+}
+__device__ __forceinline__ bool cl_wait_count(const Params& P, uint32_t a, uint32_t v) {
+    uint32_t c;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(c) : "r"(a) : "memory");
+    if (c >= v) return true;
+    return cl_wait_count_slow(a, v, P.timeout_ns, P.err);
+}
 
 // Shared memory of one cluster-ring CTA (dynamic; byte offsets):
 //   inbox [kClStages][kClStageBytes]  written by the predecessor (st.async)
@@ -197,19 +254,35 @@ __device__ __forceinline__ bool cl_wait(const Params& P, uint32_t bar, uint32_t 
 // so a warp's 16-B accesses are contiguous (no 32-B stride bank conflicts).
 // Compute warps only touch local barriers; the one remote arrive per tile (the
 // credit) is the signal warp's, off the data path.
+// With POLAR_CL_AGL2 (all-gather through L2):
+//   agst  [kClAgF + kClAgP][kClStageBytes]  final tiles, then pulled tiles, on
+//                  their way to my buffer
+//   finfull[kClAgF] my compute warps wrote a final tile into the stage (kClWarps arrivals)
+//   loaded [kClAgP] the predecessor's tile landed (1 arrival + tx; pull warp)
+//   cnt            tiles the predecessor has published in its buffer (u32,
+//                  written by the predecessor's pull warp)
+//   finok          final tiles whose stage the store warp has handed out (u32)
+//   findone        final tiles whose stores completed (u32, store warp -> pull warp)
 struct ClRingSmem {
     uint32_t inbox, own, full, cons, empty, ofull, oempty, fin;
+    uint32_t agst, finfull, loaded, cnt, finok, findone;
 };
 __device__ __forceinline__ ClRingSmem cl_ring_smem(uint32_t base) {
     ClRingSmem s;
     s.inbox = base;
     s.own = base + (uint32_t)(kClStages * kClStageBytes);
-    s.full = s.own + (uint32_t)(kClOwn * kClStageBytes);
+    s.agst = s.own + (uint32_t)(kClOwn * kClStageBytes);
+    s.full = s.agst + (uint32_t)(kClAg * kClStageBytes);
     s.cons = s.full + 8u * kClStages;
     s.empty = s.cons + 8u * kClStages;
     s.ofull = s.empty + 8u * kClStages;
     s.oempty = s.ofull + 8u * kClOwn;
-    s.fin = s.oempty + 8u * kClOwn;
+    s.finfull = s.oempty + 8u * kClOwn;
+    s.loaded = s.finfull + 8u * kClAgF;
+    s.fin = s.loaded + 8u * kClAgP;
+    s.cnt = s.fin + 8u;
+    s.finok = s.cnt + 4u;
+    s.findone = s.finok + 4u;
     return s;
 }
 __device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
@@ -217,6 +290,10 @@ __device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
     asm volatile("mbarrier.arrive." POLAR_CL_SEM ".cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// release (CTA scope): my shared-memory writes before it are visible to the waiter
+__device__ __forceinline__ void mbar_arrive_rel_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_u32(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx." POLAR_CL_SEM ".cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
@@ -301,7 +378,15 @@ __device__ __forceinline__ bool cl_ring_walk(int r, int n, unsigned long long ca
 // next RECEIVED tile (steps s >= 1) at or after q
 __device__ __forceinline__ void ring_cursor_recv(RingCursor& q, int r, int n, unsigned long long cb,
                                                  unsigned long long SP, unsigned TP) {
-    while (!q.done && q.s == 0) ring_cursor_next(q, r, n, cb, SP, TP);
+    // (all-gather through L2: only the reduce-scatter steps 1..n-1 receive via DSMEM)
+    while (!q.done && (q.s == 0 || (kClAgL2 && q.s >= n))) ring_cursor_next(q, r, n, cb, SP, TP);
+}
+// next all-gather item (POLAR_CL_AGL2): the final step's tiles (s = n-1,
+// produced by my compute warps) and the all-gather steps' tiles (s >= n,
+// pulled from the predecessor's buffer), in walk order
+__device__ __forceinline__ void ring_cursor_ag(RingCursor& q, int r, int n, unsigned long long cb,
+                                               unsigned long long SP, unsigned TP) {
+    while (!q.done && q.s < n - 1) ring_cursor_next(q, r, n, cb, SP, TP);
 }
 
 // Sub-chunk size: the FIFO ring's slot (same geometry => same reduction order),
@@ -320,7 +405,7 @@ template <int AW> __device__ __forceinline__ unsigned long long cl_ring_sp(const
 //   fin    s = n-1      fin(inbox (op) own) -> HBM + successor  (1 word)
 //   ag     n-1 < s < 2(n-1)   inbox (1) -> HBM + successor
 //   last   s = 2(n-1)   inbox (1) -> HBM
-enum { kClFirst = 0, kClMid = 1, kClFin = 2, kClAg = 3, kClLast = 4 };
+enum { kClFirst = 0, kClMid = 1, kClFin = 2, kClAgStep = 3, kClLast = 4 };
 
 // The compute warps' state and per-step tile loop.  Stage indices and phase
 // parities are 32-bit counters that wrap (no 64-bit division per tile); each
@@ -339,14 +424,18 @@ struct ClCompute {
     uint32_t xo = 0, pe = 1;        // successor stage / parity of its credit phase
     uint32_t xw = 0, pw = 0;        // own stage / parity
     bool wrapped = false;           // sent >= kClStages: credits are needed
+    unsigned long long ag_item = 0; // POLAR_CL_AGL2: final tiles staged so far
 
     // One tile: every shared-memory load of the lane's PPL packs first, then
     // the arithmetic, then the stores (one register set per pack: loads of later
     // packs are not serialised behind the stores of earlier ones).
+    // (POLAR_CL_AGL2, final step: `dst` is the local all-gather stage; the
+    // result goes there, and the all-gather warp stores it and publishes it)
     template <int KIND, bool FULL>
     __device__ __forceinline__ void body(uint32_t in, uint32_t ow, uint32_t dst, uint32_t dbar, uint4* gout,
                                          unsigned npk) {
-        constexpr bool SEND = KIND != kClLast, OWN = KIND <= kClFin, OUT = KIND >= kClFin;
+        constexpr bool STAGE = kClAgL2 && KIND == kClFin;
+        constexpr bool SEND = KIND != kClLast && !STAGE, OWN = KIND <= kClFin, OUT = KIND >= kClFin && !STAGE;
         constexpr int WIN = (KIND == kClMid || KIND == kClFin) ? AW : (KIND == kClFirst ? 0 : 1);
         constexpr int WOUT = KIND <= kClMid ? AW : 1;
         uint4 o[PPL], a[PPL][AW > 1 ? AW : 1];
@@ -382,6 +471,10 @@ struct ClCompute {
             } else {
                 v = a[u][0];
             }
+            if constexpr (STAGE)
+                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst + p * 16u), "r"(v.x), "r"(v.y),
+                             "r"(v.z), "r"(v.w)
+                             : "memory");
             if constexpr (OUT) {
                 if (POLAR_CL_ABL != 2) st_plain(gout + p, v);
             }
@@ -391,26 +484,37 @@ struct ClCompute {
 
     template <int KIND>
     __device__ __forceinline__ bool tiles(const Params& P, unsigned long long ks, unsigned long long ke) {
-        constexpr bool RECV = KIND != kClFirst, SEND = KIND != kClLast;
+        constexpr bool STAGE = kClAgL2 && KIND == kClFin;
+        constexpr bool RECV = KIND != kClFirst, SEND = KIND != kClLast && !STAGE;
         constexpr bool OWN = KIND <= kClFin;
         for (unsigned long long i0 = ks; i0 < ke; i0 += TP) {
             const unsigned npk = (unsigned)((ke - i0) < TP ? (ke - i0) : TP);
             if (RECV && !cl_wait(P, S.full + 8u * xi, pi)) return false;
             if (OWN && !cl_wait(P, S.ofull + 8u * xw, pw)) return false;
             if (SEND && wrapped && !cl_wait(P, S.empty + 8u * xo, pe)) return false;
+            uint32_t xa = 0;
+            if constexpr (STAGE) {
+                // the store warp has handed this final tile its stage (the
+                // stage's previous tile has been read by its bulk store)
+                xa = (uint32_t)(ag_item % kClAgF);
+                if (!cl_wait_count(P, S.finok, (uint32_t)(ag_item + 1))) return false;
+            }
             const uint32_t in = S.inbox + xi * (uint32_t)kClStageBytes;
             const uint32_t ow = S.own + xw * (uint32_t)kClStageBytes;
-            const uint32_t dst = dst_inbox + xo * (uint32_t)kClStageBytes;
+            const uint32_t dst = STAGE ? S.agst + xa * (uint32_t)kClStageBytes : dst_inbox + xo * (uint32_t)kClStageBytes;
             const uint32_t dbar = dst_full + 8u * xo;
             uint4* gout = mine + i0;
             if (SEND) jitter_warp(P);
             if (npk == TP) body<KIND, true>(in, ow, dst, dbar, gout, npk);
             else body<KIND, false>(in, ow, dst, dbar, gout, npk);
+            if constexpr (STAGE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // -> the bulk store
             __syncwarp();
             if ((me & 31u) == 0) {
                 if (RECV) mbar_arrive_u32(S.cons + 8u * xi);   // my reads of the inbox stage are done
                 if (OWN) mbar_arrive_u32(S.oempty + 8u * xw);
+                if (STAGE) mbar_arrive_rel_u32(S.finfull + 8u * xa);
             }
+            if (STAGE) ++ag_item;
             if (RECV && ++xi == (uint32_t)kClStages) { xi = 0; pi ^= 1u; }
             if (OWN && ++xw == (uint32_t)kClOwn) { xw = 0; pw ^= 1u; }
             if (SEND && ++xo == (uint32_t)kClStages) { xo = 0; pe ^= 1u; wrapped = true; }
@@ -418,6 +522,219 @@ struct ClCompute {
         return true;
     }
 };
+
+// All-gather through L2 (POLAR_CL_AGL2; DESIGN.md §8 "Cluster transport").
+// The ring's all-gather forwards each final sub-chunk from rank to rank; here a
+// hop is a pull: at all-gather step s I copy sub-chunk k(s) from my
+// predecessor's buffer — where it stored that sub-chunk one step earlier — to
+// mine, with a TMA load into a shared-memory stage and a TMA store out of it.
+// The final step's tiles come from my compute warps through the same stages.
+// After a tile's store has completed (bulk async-group) I publish it: a
+// release store of "tiles readable in my buffer" into my successor's shared
+// memory, which its all-gather warp polls before pulling.  DSMEM then carries
+// only the reduce-scatter partials; the all-gather moves through L2, where my
+// predecessor's tiles were just written.  Lane 0 drives the pipeline; the warp
+// stays converged.
+__device__ __forceinline__ uint32_t cl_ld_acquire_u32(uint32_t a) {
+    uint32_t v;
+#if POLAR_CL_PUBREL
+    asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+#else
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+#endif
+    return v;
+}
+// Publication of all-gather tiles: a relaxed store of the count into the
+// successor's shared memory, after the tiles' bulk stores have completed
+// (cp.async.bulk.wait_group: the writes are performed in L2, where the
+// successor's bulk loads read them).  A release store / acquire load at
+// cluster scope was measured at ~75 us per publication (it drains far more
+// than this thread's completed stores; 8 MiB 27.7 -> 3.8 ms) — the ordering it
+// would add is already given by the completed bulk group.
+#ifndef POLAR_CL_PUBREL
+#define POLAR_CL_PUBREL 0
+#endif
+#ifndef POLAR_CL_PUBFENCE
+#define POLAR_CL_PUBFENCE 0
+#endif
+__device__ __forceinline__ void cl_st_release_remote_u32(uint32_t ra, uint32_t v) {
+#if POLAR_CL_PUBREL
+    asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+#else
+    asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+#endif
+}
+__device__ __forceinline__ void bulk_store_u32(void* gdst, uint32_t ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
+                 : "memory");
+}
+// final tiles (step n-1) in walk order: stage in my compute warps' hands ->
+// bulk store into my buffer; hands the stage back once its store has read it;
+// publishes "final tiles stored" (findone) for the pull warp's prefix count
+template <int AW>
+__device__ __noinline__ void cl_ring_fin_warp(const Params& P, const ClRingSmem S, int r, int n, unsigned long long ca,
+                                              unsigned long long cb, unsigned long long SP, uint4* mine, int lane) {
+    constexpr unsigned TP = cl_tile<AW>();
+    constexpr int F = kClAgF > 0 ? kClAgF : 1;
+    RingCursor q = ring_cursor(r, n, ca, cb, SP);
+    uint32_t j = 0;
+    for (;;) {
+        while (!q.done && q.s != n - 1) ring_cursor_next(q, r, n, cb, SP, TP);
+        if (q.done) break;
+        const uint32_t x = j % F;
+        if (!__all_sync(0xffffffffu, cl_wait(P, S.finfull + 8u * x, (j / F) & 1u))) break;
+        if (lane == 0) {
+            bulk_store_u32(mine + q.i0, S.agst + x * (uint32_t)kClStageBytes, ring_cursor_npk(q, TP) * 16u);
+            bulk_commit();
+            bulk_wait_read<0>();   // the stage may be refilled
+            asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(S.finok), "r"(j + 1 + F) : "memory");
+            // completed stores: all of them if the next tile is not ready yet, else all but this one
+            const bool idle = !cl_try_wait(S.finfull + 8u * ((j + 1) % F), ((j + 1) / F) & 1u);
+            if (idle) bulk_wait_all();
+            else bulk_wait_group<1>();
+            asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(S.findone), "r"(idle ? j + 1 : j) : "memory");
+        }
+        __syncwarp();
+        ++j;
+        ring_cursor_next(q, r, n, cb, SP, TP);
+    }
+    if (lane == 0) {
+        bulk_wait_all();
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(S.findone), "r"(j) : "memory");
+    }
+    __syncwarp();
+}
+
+// Walk-order publication: how many of my readable tiles (final tiles and the
+// pulled tiles of steps n .. 2n-3, lap by lap in walk order) are in my buffer,
+// given the final tiles stored (fdone) and the pulled tiles stored (pdone).
+struct PubCursor {
+    RingCursor q;
+    uint32_t fi = 0, pi = 0, readable = 0;
+    __device__ __forceinline__ void advance(int r, int n, unsigned long long cb, unsigned long long SP, unsigned TP,
+                                            uint32_t fdone, uint32_t pdone) {
+        for (;;) {
+            while (!q.done && q.s < n - 1) ring_cursor_next(q, r, n, cb, SP, TP);
+            if (q.done) return;
+            if (q.s == n - 1) {
+                if (fi >= fdone) return;
+                ++fi;
+                ++readable;
+            } else {
+                if (pi >= pdone) return;
+                ++pi;
+                if (q.s <= 2 * (n - 1) - 1) ++readable;
+            }
+            ring_cursor_next(q, r, n, cb, SP, TP);
+        }
+    }
+};
+
+// pulled tiles (steps n .. 2(n-1)) in walk order: wait until the predecessor
+// published the tile, bulk load it from the predecessor's buffer into a stage,
+// bulk store it into mine; publish the walk-order prefix to the successor
+template <int AW>
+__device__ __noinline__ void cl_ring_pull_warp(const Params& P, const ClRingSmem S, int r, int n,
+                                               unsigned long long ca, unsigned long long cb, unsigned long long SP,
+                                               uint4* mine, const uint4* pred_buf, uint32_t succ_cnt, int lane) {
+    constexpr unsigned TP = cl_tile<AW>();
+    constexpr int A = kClAgP > 0 ? kClAgP : 1;
+    constexpr int LAG = kClAgLag;
+    auto next_pull = [&](RingCursor& c) {
+        while (!c.done && c.s < n) ring_cursor_next(c, r, n, cb, SP, TP);
+    };
+    RingCursor ci = ring_cursor(r, n, ca, cb, SP), cs = ci;   // issue / store cursors
+    next_pull(ci);
+    next_pull(cs);
+    PubCursor pub;
+    pub.q = ring_cursor(r, n, ca, cb, SP);
+    uint32_t m_iss = 0, m_sto = 0, seen = 0, published = 0, ldpar = 0;
+    unsigned long long t0 = 0;
+    uint32_t spins = 0;
+    bool ok = true;
+    auto publish = [&](uint32_t pdone) {
+        uint32_t fdone = 0;
+        if (lane == 0) asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(fdone) : "r"(S.findone) : "memory");
+        fdone = __shfl_sync(0xffffffffu, fdone, 0);
+        pub.advance(r, n, cb, SP, TP, fdone, pdone);
+        if (pub.readable != published) {
+            if (lane == 0) cl_st_release_remote_u32(succ_cnt, pub.readable);
+            published = pub.readable;
+        }
+        __syncwarp();
+    };
+    while (ok) {
+        // ---- issue loads ahead, as the predecessor's count allows
+        while (!ci.done && m_iss < m_sto + A) {
+            if (seen < m_iss + 1) {
+                uint32_t v = 0;
+                if (lane == 0) v = cl_ld_acquire_u32(S.cnt);
+                seen = __shfl_sync(0xffffffffu, v, 0);
+                if (seen < m_iss + 1) break;
+            }
+            const uint32_t y = m_iss % A;
+            if (lane == 0) {
+                if (m_iss >= (uint32_t)A) bulk_wait_read<0>();   // the stage's previous store has read it
+                const unsigned npk = ring_cursor_npk(ci, TP);
+                mbar_expect_u32(S.loaded + 8u * y, npk * 16u);
+                bulk_load_u32(S.agst + (uint32_t)(kClAgF + y) * (uint32_t)kClStageBytes, pred_buf + ci.i0, npk * 16u,
+                              S.loaded + 8u * y);
+            }
+            __syncwarp();
+            ++m_iss;
+            ring_cursor_next(ci, r, n, cb, SP, TP);
+            next_pull(ci);
+        }
+        if (cs.done) break;
+        if (m_sto == m_iss) {
+            // nothing loaded: publish what is stored, then wait for the predecessor
+            if (lane == 0) bulk_wait_all();
+            __syncwarp();
+            publish(m_sto);
+            if (t0 == 0) t0 = globaltimer();
+            if ((++spins & 255) == 0 && (globaltimer() - t0 > P.timeout_ns || *(volatile int*)P.err)) {
+                if (lane == 0 && !*(volatile int*)P.err) raise_error(P, POLAR_ETIMEOUT);
+                ok = false;
+            }
+            continue;
+        }
+        t0 = 0;
+        // ---- store the oldest loaded tile
+        const uint32_t y = m_sto % A;
+        if (!__all_sync(0xffffffffu, cl_wait(P, S.loaded + 8u * y, (ldpar >> y) & 1u))) break;
+        ldpar ^= 1u << y;
+        if (lane == 0) {
+            bulk_store_u32(mine + cs.i0, S.agst + (uint32_t)(kClAgF + y) * (uint32_t)kClStageBytes,
+                           ring_cursor_npk(cs, TP) * 16u);
+            bulk_commit();
+        }
+        __syncwarp();
+        ++m_sto;
+        ring_cursor_next(cs, r, n, cb, SP, TP);
+        next_pull(cs);
+        // ---- publish the tiles whose stores completed (all but the LAG newest)
+        if (m_sto > (uint32_t)LAG) {
+            if (lane == 0) bulk_wait_group<LAG>();
+            __syncwarp();
+            publish(m_sto - LAG);
+        }
+    }
+    // the final publication covers every tile, the last final tiles included
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+    if (ok) {
+        const unsigned long long tw = globaltimer();
+        for (;;) {
+            publish(m_sto);
+            if (pub.q.done) break;
+            if (globaltimer() - tw > P.timeout_ns) {
+                if (lane == 0) raise_error(P, POLAR_ETIMEOUT);
+                break;
+            }
+        }
+    }
+}
+
 
 template <int DT, int OP>
 __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel(Params P) {
@@ -453,6 +770,12 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
             mbar_init_u32(S.ofull + 8u * x, 1);
             mbar_init_u32(S.oempty + 8u * x, kClWarps);
         }
+        for (int x = 0; x < kClAgF; ++x) mbar_init_u32(S.finfull + 8u * x, kClWarps);
+        for (int x = 0; x < kClAgP; ++x) mbar_init_u32(S.loaded + 8u * x, 1);
+        if (kClAgL2)
+            asm volatile("st.shared.u32 [%0], 0;\n\tst.shared.u32 [%1], %3;\n\tst.shared.u32 [%2], 0;" ::"r"(S.cnt),
+                         "r"(S.finok), "r"(S.findone), "n"(kClAgF)
+                         : "memory");
         mbar_init_u32(S.fin, (uint32_t)(n - 1));
         mbar_fence_init();
         // arm the first kClStages received tiles
@@ -521,7 +844,7 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
             ring_cursor_next(q, r, n, cb, SP, TP);
             ++nr;
         }
-    } else {
+    } else if (warp < 2 + kClWarps) {
         // ------------------------------------------------------- compute warps
         const uint32_t succ = (uint32_t)((r + 1) % n);
         ClCompute<DT, OP> cp;
@@ -534,7 +857,8 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
         bool ok = true;
         for (unsigned long long base = ca; base < cb && ok; base += LC) {
             const unsigned long long L = (cb - base < LC) ? cb - base : LC;
-            for (int s = 0; s < 2 * (n - 1) + 1 && ok; ++s) {
+            // (all-gather through L2: the compute warps run the reduce-scatter steps only)
+            for (int s = 0; s < (kClAgL2 ? n : 2 * (n - 1) + 1) && ok; ++s) {
                 int k;
                 if (s < n) k = ((r - s) % n + n) % n;
                 else k = ((r - (s - n)) % n + n) % n;
@@ -545,10 +869,18 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
                 if (s == 0) ok = cp.template tiles<kClFirst>(P, ks, ke);
                 else if (s < n - 1) ok = cp.template tiles<kClMid>(P, ks, ke);
                 else if (s == n - 1) ok = cp.template tiles<kClFin>(P, ks, ke);
-                else if (s < 2 * (n - 1)) ok = cp.template tiles<kClAg>(P, ks, ke);
+                else if (s < 2 * (n - 1)) ok = cp.template tiles<kClAgStep>(P, ks, ke);
                 else ok = cp.template tiles<kClLast>(P, ks, ke);
             }
         }
+    } else if (warp == 2 + kClWarps) {
+        // ------------------------------------------- final-tile store warp (L2)
+        cl_ring_fin_warp<AW>(P, S, r, n, ca, cb, SP, reinterpret_cast<uint4*>(mine), lane);
+    } else {
+        // ------------------------------------------------- all-gather pull warp (L2)
+        cl_ring_pull_warp<AW>(P, S, r, n, ca, cb, SP, reinterpret_cast<uint4*>(mine),
+                              reinterpret_cast<const uint4*>(P.bufs[(r + n - 1) % n]),
+                              cl_map(S.cnt, (uint32_t)((r + 1) % n)), lane);
     }
     cl_rendezvous(P, S.fin, r, n);
     if (tel) {
