@@ -78,7 +78,7 @@ namespace dev {
 #if POLAR_CL_AGL2
 #define POLAR_CL_OWN 2            // own-input stages (TMA loads in flight)
 #else
-#define POLAR_CL_OWN 3
+#define POLAR_CL_OWN 4            // (3: 128 MiB f32 685 us, 4: 650 us; profiles/r02y_cluster_ring_ab.jsonl)
 #endif
 #endif
 constexpr int kClWarps = POLAR_CL_WARPS;
