@@ -198,6 +198,7 @@ def workload_config(n, real):
         "nranks": n, "bytes_per_rank": S_BYTES, "op": "sum", "dtype": "f32",
         "buffers": "symmetric (polar_mem_alloc: registered, zero-copy two-shot)",
         "l2": f"inputs larger than L2 ({n} x {S_BYTES >> 20} MiB resident), no flush",
+        "prewarm": "after the W warm-up steps, untimed steps for ~0.25 s (clock ramp out of idle)",
     }
 
 
@@ -375,7 +376,18 @@ def run_polar(args):
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         return float(t.item())
 
+    t_w = time.perf_counter()
     for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # clock ramp: the GPU may come out of idle (120 MHz) at the start of the run;
+    # after the W warm-up steps keep stepping (untimed) for ~0.25 s so the timed
+    # steps run at full clock (measured: with 5 warm-up steps after idle time
+    # the timed steps came out ~3 % slow).  The same count on every rank (the
+    # steps are collectives).
+    t_est = (time.perf_counter() - t_w) / max(1, args.warmup)
+    prewarm = int(max_over_ranks(float(min(4000, int(0.25 / max(t_est, 1e-5))))))
+    for _ in range(prewarm):
         step()
     torch.cuda.synchronize()
     comm.check()

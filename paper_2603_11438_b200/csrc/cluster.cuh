@@ -496,7 +496,7 @@ struct ClCompute {
             if constexpr (STAGE) {
                 // the store warp has handed this final tile its stage (the
                 // stage's previous tile has been read by its bulk store)
-                xa = (uint32_t)(ag_item % kClAgF);
+                xa = (uint32_t)(ag_item % (kClAgF > 0 ? kClAgF : 1));
                 if (!cl_wait_count(P, S.finok, (uint32_t)(ag_item + 1))) return false;
             }
             const uint32_t in = S.inbox + xi * (uint32_t)kClStageBytes;
@@ -905,6 +905,13 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
 // Full barriers are armed by the senders' warps (remote arrive.expect_tx with
 // the bytes each warp sent), credits are returned by each consuming warp: the
 // up and down groups have kTrGroup warps each, so every count is kTrGroup.
+// (Measured and not adopted: a double binary tree — half of each channel through
+// the tree with positions shifted by ceil(n/2), whose interior nodes are this
+// tree's leaves, so no SM moves more than 2 tiles per tile instead of 3.
+// Interleaved tile by tile in one pipeline every tile chains through both
+// trees: 128 MiB 5990 us; as two concurrent pipelines on disjoint warps and
+// half the shared memory each: 1184-2774 us vs 1107 us for this tree;
+// profiles/r02dd_*, r02ee_*.)
 #ifndef POLAR_TR_WIRE
 #define POLAR_TR_WIRE 1024        // 16-B wire words per stage (16 KiB)
 #endif

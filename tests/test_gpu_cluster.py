@@ -67,12 +67,13 @@ def test_cluster_matrix(algo, n, monkeypatch):
 def test_cluster_tree_matches_fifo_bitwise(dtype, monkeypatch):
     """The tree's reduction order (own (op) child0 (op) child1, root = rank c
     mod n) does not depend on tiling: for the same channel count the cluster
-    tree and the FIFO tree give the same bits (f32 / bf16 sums of real data)."""
+    tree and the FIFO tree give the same bits (f32 / bf16 sums of real data),
+    at sizes below and above the tree's default cluster bound."""
     n = 8
-    a = _comm(n, monkeypatch, cluster=True)
+    a = _comm(n, monkeypatch, cluster=True, POLAR_CLUSTER_TREE_MAX=1 << 40)
     b = _comm(n, monkeypatch, cluster=False)
     try:
-        for count, nch in ((4096, 1), (123_456, 5), (2_000_000, 15)):
+        for count, nch in ((4096, 1), (123_456, 5), (2_000_000, 15), (9_000_000, 15)):
             count = _aligned(count, dtype)
             xs = synth.gen_ranks(dtype, count, n, cfg=33, dist=default_dist(dtype))
             ta = [to_device(x, dtype) for x in xs]
@@ -82,6 +83,7 @@ def test_cluster_tree_matches_fifo_bitwise(dtype, monkeypatch):
             assert a.transport() == "cluster" and b.transport() == "peer"
             assert a.launched_channels() == b.launched_channels() == nch
             torch.cuda.synchronize()
+            a.check()
             for x, y in zip(ta, tb):
                 assert np.array_equal(to_host(x, dtype), to_host(y, dtype)), count
             check_result([to_host(t, dtype) for t in ta], xs, dtype, "sum", "tree", n)
