@@ -44,6 +44,7 @@ print("tma twoshot", "ok" if ok else "MISMATCH", flush=True)
 # TMA-staged ring Simple (opt-in kernel; round 2), with and without L2 hints + discard
 for flags in ("1", "3"):
     os.environ["POLAR_RING_TMA"] = "1"
+    os.environ["POLAR_CLUSTER"] = "0"      # aligned sizes would run as clusters
     os.environ["POLAR_RING_TMA_FLAGS"] = flags
     cr = L.Comm.virtual(n, 0)
     for dtype in ("f32", "bf16"):
@@ -57,7 +58,26 @@ for flags in ("1", "3"):
             bad += 0 if ok else 1
             print("ring tma", flags, dtype, count, "ok" if ok else "MISMATCH", flush=True)
     cr.destroy()
-    del os.environ["POLAR_RING_TMA"], os.environ["POLAR_RING_TMA_FLAGS"]
+    del os.environ["POLAR_RING_TMA"], os.environ["POLAR_RING_TMA_FLAGS"], os.environ["POLAR_CLUSTER"]
+# cluster transport (csrc/cluster.cuh): ring / tree Simple on aligned whole packs,
+# DSMEM hops between the CTAs of a cluster; n = 3 and 8, multi-lap sizes
+os.environ["POLAR_CLUSTER_TREE_MAX"] = str(1 << 40)
+for nc in (3, 8):
+    cc = L.Comm.virtual(nc, 0)
+    for dtype in ("f32", "bf16"):
+        for algo in ("ring", "tree"):
+            for count in (5_008, 300_000, 1_300_000):
+                xs = synth.gen_ranks(dtype, count, nc, cfg=8, dist="ints")
+                ts = [to_device(x, dtype) for x in xs]
+                cc.allreduce_forced(ts, algo, "simple", 3)
+                assert cc.transport() == "cluster"
+                torch.cuda.synchronize()
+                cc.check()
+                ok = all(np.array_equal(to_host(t, dtype), orc.allreduce(xs, dtype, "sum")) for t in ts)
+                bad += 0 if ok else 1
+                print("cluster", nc, dtype, algo, count, "ok" if ok else "MISMATCH", flush=True)
+    cc.destroy()
+del os.environ["POLAR_CLUSTER_TREE_MAX"]
 sends = [torch.randn(n * 1000, device="cuda") for _ in range(n)]
 recvs = [torch.empty(1000, device="cuda") for _ in range(n)]
 c.reduce_scatter(sends, recvs)
