@@ -371,7 +371,7 @@ polar_status polar_comm_launch_info(polar_comm_t comm, uint32_t* nchannels, uint
  * DESIGN.md §8 "Cluster transport").  Same algorithm, schedule and reduction
  * order either way.  POLAR_CLUSTER=0 (read at polar_comm_init_virtual) keeps
  * virtual comms on the peer transport; POLAR_CLUSTER_TREE_MAX (bytes per rank,
- * default 16 MiB) bounds the sizes that run the cluster tree. */
+ * default: no bound) bounds the sizes that run the cluster tree. */
 enum { POLAR_TRANSPORT_PEER = 0, POLAR_TRANSPORT_CLUSTER = 1 };
 polar_status polar_comm_transport(polar_comm_t comm, int* transport);
 

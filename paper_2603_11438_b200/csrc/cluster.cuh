@@ -924,22 +924,39 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
 #ifndef POLAR_TR_OWN
 #define POLAR_TR_OWN 2            // own-input stages
 #endif
+#ifndef POLAR_TR_L2DN
+#define POLAR_TR_L2DN 1
+#endif
 #ifndef POLAR_TR_GROUP
+#if POLAR_TR_L2DN
+#define POLAR_TR_GROUP 16         // up-group warps (128 MiB f32, HBM frac: 0.34 with 4, 0.52 with 8, 0.56 with 16, 0.54 with 24)
+#else
 #define POLAR_TR_GROUP 4          // warps per group (up, down)
 #endif
+#endif
+// POLAR_TR_L2DN (the default): the down phase through L2 instead of DSMEM.  The
+// root's up group stages each result tile in shared memory; one down warp
+// bulk-stores it into the root's buffer and, once the store has completed,
+// publishes the count of tiles in that buffer to each child (relaxed remote
+// store); a non-root's down warp pulls its parent's published tiles from the
+// parent's buffer with TMA loads and bulk-stores them into its own, publishing
+// in turn.  DSMEM then carries only the up phase: an interior node moves 2
+// tiles in and 1 out per tile (f32) instead of 3 and 3.
+constexpr bool kTrL2 = POLAR_TR_L2DN != 0;
 constexpr unsigned kTrWire = POLAR_TR_WIRE;
 constexpr size_t kTrStage = (size_t)kTrWire * 16;
 constexpr int kTrUp = POLAR_TR_UP, kTrDn = POLAR_TR_DN, kTrOwn = POLAR_TR_OWN, kTrGroup = POLAR_TR_GROUP;
-constexpr int kTrThreads = 32 * (1 + 2 * kTrGroup);
+constexpr int kTrThreads = 32 * (1 + kTrGroup + (kTrL2 ? 1 : kTrGroup));
 constexpr int kTrNbar = 2 * kTrUp + kTrUp + kTrDn + 2 * kTrDn + 2 * kTrOwn + 1;
 __host__ __device__ constexpr size_t cl_tree_smem_bytes() {
-    return (size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8;
+    return (size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8 + 8;
 }
 struct ClTreeSmem {
     uint32_t up[2], dn, own;            // inboxes (child k up, parent down), own stages
     uint32_t upfull[2], upempty;        // up inbox k landed / my up sends' credits
     uint32_t dnfull, dnempty[2];        // down inbox landed / my down sends to child k: credits
     uint32_t ofull, oempty, fin;
+    uint32_t cnt, stok;                 // L2 down: parent's published tiles; root staging stages handed out
 };
 __device__ __forceinline__ ClTreeSmem cl_tree_smem(uint32_t base) {
     ClTreeSmem t;
@@ -957,6 +974,8 @@ __device__ __forceinline__ ClTreeSmem cl_tree_smem(uint32_t base) {
     t.ofull = o; o += 8u * kTrOwn;
     t.oempty = o; o += 8u * kTrOwn;
     t.fin = o;
+    t.cnt = o + 8u;
+    t.stok = o + 12u;
     return t;
 }
 // a ring counter: stage index and the parity of the phase to wait for
@@ -967,6 +986,102 @@ struct StageCtr {
         if (++x == D) { x = 0; par ^= 1u; wrapped = true; }
     }
 };
+
+// The L2 down phase (POLAR_TR_L2DN), one warp, lane 0 drives:
+//   root     result tiles staged by the up group -> bulk store into my buffer
+//   non-root my parent's published tiles -> TMA load into a stage -> bulk store
+//            into my buffer
+// then, once a tile's store has completed (bulk group), publish "tiles in my
+// buffer" to each child (relaxed remote store: the completed group is what
+// orders the data; a cluster-scope release costs ~75 us here, §8).  Stages:
+// kTrDn; the root hands a staging stage back (stok) once its store has read it.
+template <int AW>
+__device__ __noinline__ void tree_down_l2(const Params& P, const ClTreeSmem S, bool root, int nchild,
+                                          const uint32_t (&ch_cnt)[2], const uint4* par_buf, uint4* mine,
+                                          unsigned long long ca, unsigned long long cb, int lane) {
+    constexpr unsigned TP = kTrWire / (unsigned)AW;
+    constexpr int D = kTrDn;
+    const uint32_t ntiles = (uint32_t)((cb - ca + TP - 1) / TP);
+    uint32_t t_iss = 0, t_sto = 0, seen = 0, published = 0, par = 0;
+    unsigned long long t0 = 0;
+    uint32_t spins = 0;
+    bool ok = true;
+    auto publish = [&](uint32_t done) {
+        if (done != published) {
+            if (lane == 0)
+                for (int k = 0; k < nchild; ++k) cl_st_release_remote_u32(ch_cnt[k], done);
+            published = done;
+        }
+        __syncwarp();
+    };
+    while (ok && t_sto < ntiles) {
+        if (!root) {
+            // issue loads ahead, as the parent's count allows
+            while (t_iss < ntiles && t_iss < t_sto + D) {
+                if (seen < t_iss + 1) {
+                    uint32_t v = 0;
+                    if (lane == 0) v = cl_ld_acquire_u32(S.cnt);
+                    seen = __shfl_sync(0xffffffffu, v, 0);
+                    if (seen < t_iss + 1) break;
+                }
+                const uint32_t x = t_iss % D;
+                const unsigned long long i0 = ca + (unsigned long long)t_iss * TP;
+                const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
+                if (lane == 0) {
+                    if (t_iss >= (uint32_t)D) bulk_wait_read<0>();   // the stage's previous store has read it
+                    mbar_expect_u32(S.dnfull + 8u * x, npk * 16u);
+                    bulk_load_u32(S.dn + x * (uint32_t)kTrStage, par_buf + i0, npk * 16u, S.dnfull + 8u * x);
+                }
+                __syncwarp();
+                ++t_iss;
+            }
+            if (t_sto == t_iss) {
+                // nothing loaded: publish what is stored, then wait for the parent
+                if (lane == 0) bulk_wait_all();
+                __syncwarp();
+                publish(t_sto);
+                if (t0 == 0) t0 = globaltimer();
+                if ((++spins & 255) == 0 && (globaltimer() - t0 > P.timeout_ns || *(volatile int*)P.err)) {
+                    if (lane == 0 && !*(volatile int*)P.err) raise_error(P, POLAR_ETIMEOUT);
+                    ok = false;
+                }
+                continue;
+            }
+            t0 = 0;
+        }
+        // store the oldest ready tile
+        const uint32_t x = t_sto % D;
+        {
+            int rd = 0;
+            if (lane == 0) rd = cl_try_wait(S.dnfull + 8u * x, (par >> x) & 1u);
+            rd = __shfl_sync(0xffffffffu, rd, 0);
+            if (!rd) {   // about to block: publish what is stored first
+                if (lane == 0) bulk_wait_all();
+                __syncwarp();
+                publish(t_sto);
+            }
+        }
+        if (!__all_sync(0xffffffffu, cl_wait(P, S.dnfull + 8u * x, (par >> x) & 1u))) break;
+        par ^= 1u << x;
+        const unsigned long long i0 = ca + (unsigned long long)t_sto * TP;
+        const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
+        if (lane == 0) {
+            bulk_store_u32(mine + i0, S.dn + x * (uint32_t)kTrStage, npk * 16u);
+            bulk_commit();
+            if (root) {
+                bulk_wait_read<0>();   // hand the staging stage back to the up group
+                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(S.stok), "r"(t_sto + 1 + D) : "memory");
+            }
+            bulk_wait_group<1>();      // all but this store have completed
+        }
+        __syncwarp();
+        publish(t_sto);
+        ++t_sto;
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+    if (ok) publish(t_sto);
+}
 
 template <int DT, int OP>
 __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
@@ -1001,7 +1116,9 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
             mbar_init_u32(S.upempty + 8u * x, kTrGroup);
         }
         for (int x = 0; x < kTrDn; ++x) {
-            mbar_init_u32(S.dnfull + 8u * x, kTrGroup);
+            // L2 down: the root's staging stages are filled by its up group, a
+            // non-root's pull stages by one TMA load each
+            mbar_init_u32(S.dnfull + 8u * x, (kTrL2 && !root) ? 1u : (uint32_t)kTrGroup);
             mbar_init_u32(S.dnempty[0] + 8u * x, kTrGroup);
             mbar_init_u32(S.dnempty[1] + 8u * x, kTrGroup);
         }
@@ -1009,6 +1126,9 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
             mbar_init_u32(S.ofull + 8u * x, 1);
             mbar_init_u32(S.oempty + 8u * x, kTrGroup);
         }
+        if (kTrL2)
+            asm volatile("st.shared.u32 [%0], 0;\n\tst.shared.u32 [%1], %2;" ::"r"(S.cnt), "r"(S.stok), "n"(kTrDn)
+                         : "memory");
         mbar_init_u32(S.fin, (uint32_t)(n - 1));
         mbar_fence_init();
     }
@@ -1064,16 +1184,21 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
         const int gw = warp - 1;
         const unsigned me = (unsigned)gw * 32u + (unsigned)lane;
         StageCtr w, in, up, dn;   // own stage, child up inboxes (both children in step), my up sends, my down sends
+        uint32_t jt = 0;          // tiles done
         for (unsigned long long i0 = ca; i0 < cb; i0 += TP) {
             const unsigned npk = (unsigned)((cb - i0) < TP ? (cb - i0) : TP);
             if (!cl_wait(P, S.ofull + 8u * w.x, w.par)) break;
             bool ok = true;
             for (int k = 0; k < nchild; ++k) ok = ok && cl_wait(P, S.upfull[k] + 8u * in.x, in.par);
             if (!root && up.wrapped) ok = ok && cl_wait(P, S.upempty + 8u * up.x, up.par ^ 1u);
-            if (root)
+            if (root && !kTrL2)
                 for (int k = 0; k < nchild; ++k)
                     if (dn.wrapped) ok = ok && cl_wait(P, S.dnempty[k] + 8u * dn.x, dn.par ^ 1u);
+            // L2 down: the root stages its result tile for the down warp (a
+            // monotone hand-out count, no parity to alias)
+            if (root && kTrL2) ok = ok && cl_wait_count(P, S.stok, jt + 1);
             if (!ok) break;
+            const uint32_t stg = S.dn + (uint32_t)(jt % kTrDn) * (uint32_t)kTrStage;
             const uint32_t ow = S.own + w.x * (uint32_t)kTrStage;
             const uint32_t cin0 = S.up[0] + in.x * (uint32_t)kTrStage, cin1 = S.up[1] + in.x * (uint32_t)kTrStage;
             const uint32_t dst = par_up + up.x * (uint32_t)kTrStage, dbar = par_upfull + 8u * up.x;
@@ -1090,7 +1215,12 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
                     for (int q = 0; q < AW; ++q) chv.w[q] = ld_shared_v4((k ? cin1 : cin0) + ((unsigned)q * TP + p) * 16u);
                     acc_merge<DT, OP>(acc, chv);
                 }
-                if (root) {
+                if (root && kTrL2) {
+                    const uint4 v = acc_fin<DT>(acc);
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(stg + p * 16u), "r"(v.x), "r"(v.y),
+                                 "r"(v.z), "r"(v.w)
+                                 : "memory");
+                } else if (root) {
                     const uint4 v = acc_fin<DT>(acc);
                     st_plain(mine + i0 + p, v);
                     for (int k = 0; k < nchild; ++k) cl_st_async(ch_dn[k] + dn.x * (uint32_t)kTrStage + p * 16u, v,
@@ -1100,19 +1230,30 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
                     for (int q = 0; q < AW; ++q) cl_st_async(dst + ((unsigned)q * TP + p) * 16u, acc.w[q], dbar);
                 }
             }
+            if (root && kTrL2) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // -> the bulk store
             __syncwarp();
             if (lane == 0) {
                 const uint32_t cnt = warp_packs(gw, npk);
                 mbar_arrive_u32(S.oempty + 8u * w.x);
                 for (int k = 0; k < nchild; ++k) cl_arrive_remote(ch_upempty[k] + 8u * in.x);   // credits to children
                 if (!root) cl_arrive_expect_remote(dbar, cnt * 16u * (uint32_t)AW);
+                else if (kTrL2) mbar_arrive_rel_u32(S.dnfull + 8u * (jt % kTrDn));
                 else
                     for (int k = 0; k < nchild; ++k) cl_arrive_expect_remote(ch_dnfull[k] + 8u * dn.x, cnt * 16u);
             }
+            ++jt;
             w.next(kTrOwn);
             if (nchild) in.next(kTrUp);
             if (!root) up.next(kTrUp);
             else if (nchild) dn.next(kTrDn);
+        }
+    } else if (kTrL2) {
+        // ------------------------------------------------ down warp (L2 down)
+        if (warp == 1 + kTrGroup) {
+            uint32_t ch_cnt[2] = {0, 0};
+            for (int k = 0; k < nchild; ++k) ch_cnt[k] = cl_map(S.cnt, (uint32_t)child[k]);
+            tree_down_l2<AW>(P, S, root, nchild, ch_cnt, root ? nullptr : reinterpret_cast<const uint4*>(P.bufs[parent]),
+                             mine, ca, cb, lane);
         }
     } else if (!root) {
         // --------------------------------------------------------- down group

@@ -164,7 +164,7 @@ struct polar_comm_s {
     // that fit on the GPU at once (cudaOccupancyMaxActiveClusters)
     bool cluster = false;
     int cl_max_ch[5] = {};               // per algorithm id
-    size_t cl_tree_max = 16u << 20;      // cluster tree up to this many bytes per rank (POLAR_CLUSTER_TREE_MAX)
+    size_t cl_tree_max = ~(size_t)0;     // cluster tree up to this many bytes per rank (POLAR_CLUSTER_TREE_MAX)
     std::mutex mu;
 };
 
@@ -1037,11 +1037,10 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
     if (st == POLAR_OK && nranks > 1) {
         const char* ec = std::getenv("POLAR_CLUSTER");
         c->cluster = !(ec && ec[0] == '0');
-        // The cluster tree's interior nodes carry 3 S of DSMEM traffic each way
-        // (up: 2 children in, 1 out; down: 1 in, 2 out) through one SM's port:
-        // faster than the FIFO tree up to 16-32 MiB per rank, slower above
-        // (DESIGN.md §8 "Cluster transport"; profiles/r02aa_cluster_tree_ab.jsonl)
-        c->cl_tree_max = env_size("POLAR_CLUSTER_TREE_MAX", 16u << 20);
+        // The cluster tree (down phase through L2) is faster than the FIFO tree at
+        // every size measured (DESIGN.md §8 "Cluster transport"); the bound stays
+        // as a knob (POLAR_CLUSTER_TREE_MAX bytes per rank, default: none)
+        c->cl_tree_max = env_size("POLAR_CLUSTER_TREE_MAX", ~(size_t)0);
         for (int algo : {POLAR_ALGO_RING, POLAR_ALGO_TREE})
             c->cl_max_ch[algo] = c->cluster ? std::min(POLAR_MAXCH, cluster_max_active(algo, nranks)) : 0;
     }
