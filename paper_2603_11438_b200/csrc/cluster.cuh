@@ -71,9 +71,6 @@ namespace dev {
 #ifndef POLAR_CL_MINB
 #define POLAR_CL_MINB 1           // CTAs per SM the register budget is sized for
 #endif
-#ifndef POLAR_CL_PROF
-#define POLAR_CL_PROF 0           // diagnostic wait-time counters into P.trace
-#endif
 #ifndef POLAR_CL_OWN
 #if POLAR_CL_AGL2
 #define POLAR_CL_OWN 2            // own-input stages (TMA loads in flight)
@@ -116,9 +113,6 @@ __device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
-#ifndef POLAR_CL_ABL
-#define POLAR_CL_ABL 0            // diagnostic ablation: 2 = no HBM result stores
-#endif
 __device__ __forceinline__ void cl_st_async(uint32_t raddr, uint4 v, uint32_t rbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(raddr),
                  "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
@@ -146,45 +140,22 @@ __device__ __forceinline__ void cl_arrive_expect_remote(uint32_t rbar, uint32_t 
                  "r"(bytes)
                  : "memory");
 }
-// POLAR_CL_WAIT: 0 = mbarrier.try_wait (may suspend the thread until the phase
-// completes or a system time limit), 1 = mbarrier.test_wait spin (never
-// suspends), 2 = try_wait with an explicit suspend-time hint (POLAR_CL_HINT ns)
-#ifndef POLAR_CL_WAIT
-#define POLAR_CL_WAIT 0
-#endif
-#ifndef POLAR_CL_HINT
-#define POLAR_CL_HINT 1000
-#endif
 // Waits are acquire.CTA (the default): acquire.cluster compiles to a
 // CCTL.IVALL (whole-L1 invalidation) after every successful wait, which the
 // compute warps paid once per tile.  Nothing here reads global memory that a
-// peer wrote: inbox data arrives through st.async, whose bytes are complete
-// when the mbarrier phase completes (complete_tx), and credits order nothing
-// but shared-memory reuse.
+// peer wrote through the generic proxy: inbox data arrives through st.async,
+// whose bytes are complete when the mbarrier phase completes (complete_tx),
+// and credits order nothing but shared-memory reuse.  (Measured:
+// mbarrier.test_wait spinning and try_wait with an explicit suspend-time hint
+// were no faster; profiles/r02t_cluster_wait_variants.jsonl.)
 __device__ __forceinline__ bool cl_try_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
-#if POLAR_CL_WAIT == 1
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
-        "p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-#elif POLAR_CL_WAIT == 2
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, "
-        "0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "n"(POLAR_CL_HINT)
-        : "memory");
-#else
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
         "p;\n}"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
-#endif
     return ok != 0;
 }
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
@@ -476,7 +447,7 @@ struct ClCompute {
                              "r"(v.z), "r"(v.w)
                              : "memory");
             if constexpr (OUT) {
-                if (POLAR_CL_ABL != 2) st_plain(gout + p, v);
+                st_plain(gout + p, v);
             }
             if constexpr (SEND) cl_st_async(dst + p * 16u, v, dbar);
         }
