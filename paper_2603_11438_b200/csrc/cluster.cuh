@@ -413,7 +413,7 @@ struct ClCompute {
 #pragma unroll
         for (unsigned u = 0; u < PPL; ++u) {
             const unsigned p = u * NT + me;
-            if (!FULL && p >= npk) continue;
+            if ((!FULL || TP % NT != 0) && p >= npk) continue;   // (a warp count that does not divide TP)
             if constexpr (OWN) o[u] = ld_shared_v4(ow + p * 16u);
 #pragma unroll
             for (int q = 0; q < WIN; ++q) a[u][q] = ld_shared_v4(in + ((unsigned)q * TP + p) * 16u);
@@ -421,7 +421,7 @@ struct ClCompute {
 #pragma unroll
         for (unsigned u = 0; u < PPL; ++u) {
             const unsigned p = u * NT + me;
-            if (!FULL && p >= npk) continue;
+            if ((!FULL || TP % NT != 0) && p >= npk) continue;   // (a warp count that does not divide TP)
             uint4 v = make_uint4(0, 0, 0, 0);
             if constexpr (OWN) {
                 Acc<DT> acc;
