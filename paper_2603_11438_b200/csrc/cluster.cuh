@@ -53,11 +53,12 @@ namespace dev {
 #ifndef POLAR_CL_STAGES
 #if POLAR_CL_AGL2
 #define POLAR_CL_STAGES 8         // ring inbox stages (>= tiles per ring step + slack)
-#define POLAR_CL_SLACK 2
 #else
 #define POLAR_CL_STAGES 10
-#define POLAR_CL_SLACK 4
 #endif
+#endif
+#ifndef POLAR_CL_SLACK
+#define POLAR_CL_SLACK (POLAR_CL_AGL2 ? 2 : 3)   // inbox stages beyond one ring step (4: 650 us, 3: 645 us f32; 896 / 885 bf16)
 #endif
 #ifndef POLAR_CL_AGP
 #define POLAR_CL_AGP 2            // all-gather pull stages (POLAR_CL_AGL2)
