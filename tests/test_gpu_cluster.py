@@ -113,6 +113,30 @@ def test_fifo_ring_tree_aligned_matrix(monkeypatch):
             c.destroy()
 
 
+@pytest.mark.parametrize("algo", ["ring", "tree"])
+def test_cluster_empty_channels_and_tiny(algo, monkeypatch):
+    """More channels than packs (most clusters get an empty slice and go
+    straight to the rendezvous), one pack, one tile plus one pack, and a
+    ragged last tile, back to back without host sync."""
+    for n in (2, 8):
+        c = _comm(n, monkeypatch)
+        try:
+            pending = []
+            for dtype, count, nch in (("f32", 4, 15), ("bf16", 8, 15), ("i64", 64, 15), ("f32", 4100, 9),
+                                      ("bf16", 8200, 3), ("i32", 1024 * 4 + 4, 1)):
+                xs = synth.gen_ranks(dtype, count, n, cfg=71, dist=default_dist(dtype))
+                ts = [to_device(x, dtype) for x in xs]
+                c.allreduce_forced(ts, algo, "simple", nch)
+                assert c.transport() == "cluster"
+                pending.append((xs, ts, dtype))
+            torch.cuda.synchronize()
+            c.check()
+            for xs, ts, dtype in pending:
+                check_result([to_host(t, dtype) for t in ts], xs, dtype, "sum", algo, n)
+        finally:
+            c.destroy()
+
+
 def test_cluster_dispatch_rule(monkeypatch):
     """Which calls run as clusters (polar.h polar_comm_transport): ring / tree
     Simple on aligned whole packs; not LL / LL128, not a partial last pack, not
