@@ -150,6 +150,7 @@ struct polar_comm_s {
     // unregistered two-shot: copy-in / kernel / copy-out pipeline over the two
     // halves of the bounce region (created on first use)
     cudaStream_t bs_in = nullptr, bs_out = nullptr;
+    bool bounce_full = false;            // POLAR_BOUNCE_FULL=1: bounce the own shard too (A/B)
     cudaEvent_t be_start = nullptr, be_in[2] = {}, be_k[2] = {}, be_out[2] = {};
     cudaEvent_t he_start = nullptr, he_in = nullptr, he_red = nullptr, he_out = nullptr;
     unsigned long long probe_epoch = 0;  // p2p probe calls (same count on every rank)
@@ -399,6 +400,10 @@ polar_status alloc_common(polar_comm_s* c) {
         const char* er = std::getenv("POLAR_RING_TMA");
         c->ring_tma = er && er[0] == '1';
         c->ring_tma_min = env_size("POLAR_RING_TMA_MIN", 0);
+        {
+            const char* eb = std::getenv("POLAR_BOUNCE_FULL");
+            c->bounce_full = eb && eb[0] == '1';
+        }
         {
             const char* ef = std::getenv("POLAR_RING_TMA_FLAGS");
             if (ef && *ef) c->ring_flags = (int)std::strtol(ef, nullptr, 0);
@@ -821,6 +826,14 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     const size_t half = (c->L.bounce_bytes / 2) & ~(size_t)15;
     const size_t chunk_elems = std::max<size_t>(16 / es, (half / es) / (16 / es) * (16 / es));
     P.vec = 1;   // the bounce halves are 16-B aligned on every rank
+    // My own shard never needs the bounce: as its owner I read it from the user
+    // buffer and store its result there (P.bufs[rank0] = the user buffer); only
+    // the shards my peers own travel through my bounce half — copied in, reduced
+    // by their owners in place, copied out.  That saves 2 · S/n of local copies
+    // per call (half of them at n = 2).  Needs a 16-B aligned user buffer (the
+    // kernel's fast path); otherwise the whole chunk bounces.
+    const bool own_direct = (reinterpret_cast<uintptr_t>(mine) % 16 == 0) && !c->bounce_full;
+    const size_t V = 16 / (size_t)es;
     CU_TRY(cudaEventRecord(c->be_start, stream));
     CU_TRY(cudaStreamWaitEvent(c->bs_in, c->be_start, 0));
     CU_TRY(cudaStreamWaitEvent(c->bs_out, c->be_start, 0));
@@ -830,8 +843,29 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         const size_t n = std::min(chunk_elems, count - done);
         char* src = mine + done * es;
         for (int p = 0; p < c->nranks; ++p) P.bufs[p] = c->scratch[p] + c->L.bounce_off + (size_t)h * half;
+        char* bnc = P.bufs[c->rank0];
+        // my shard of this chunk, in elements: the kernel's split (kernels.cuh
+        // twoshot_geo: split_range over 32-pack units)
+        size_t e0 = 0, e1 = 0;
+        if (own_direct) {
+            const size_t np = (n + V - 1) / V, units = (np + 31) / 32;
+            const size_t ua = units * (size_t)c->rank0 / (size_t)c->nranks;
+            const size_t ub = units * (size_t)(c->rank0 + 1) / (size_t)c->nranks;
+            e0 = std::min(n, ua * 32 * V);
+            e1 = std::min(n, ub * 32 * V);
+            P.bufs[c->rank0] = src;
+        }
+        auto copy_others = [&](char* dst, const char* from, cudaStream_t s) -> cudaError_t {
+            // everything but [e0, e1) (own_direct), else the whole chunk
+            cudaError_t e = cudaSuccess;
+            if (e0 > 0) e = cudaMemcpyAsync(dst, from, e0 * es, cudaMemcpyDeviceToDevice, s);
+            if (e == cudaSuccess && e1 < n)
+                e = cudaMemcpyAsync(dst + e1 * es, from + e1 * es, (n - e1) * es, cudaMemcpyDeviceToDevice, s);
+            return e;
+        };
+        if (!own_direct) e1 = 0;   // [e0, e1) empty: copy everything
         if (k >= 2) CU_TRY(cudaStreamWaitEvent(c->bs_in, c->be_out[h], 0));   // half h is free again
-        CU_TRY(cudaMemcpyAsync(P.bufs[c->rank0], src, n * es, cudaMemcpyDeviceToDevice, c->bs_in));
+        CU_TRY(copy_others(bnc, src, c->bs_in));
         CU_TRY(cudaEventRecord(c->be_in[h], c->bs_in));
         CU_TRY(cudaStreamWaitEvent(stream, c->be_in[h], 0));
         P.count = n;
@@ -840,7 +874,7 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         if (st != POLAR_OK) return st;
         CU_TRY(cudaEventRecord(c->be_k[h], stream));
         CU_TRY(cudaStreamWaitEvent(c->bs_out, c->be_k[h], 0));
-        CU_TRY(cudaMemcpyAsync(src, P.bufs[c->rank0], n * es, cudaMemcpyDeviceToDevice, c->bs_out));
+        CU_TRY(copy_others(src, bnc, c->bs_out));
         CU_TRY(cudaEventRecord(c->be_out[h], c->bs_out));
     }
     CU_TRY(cudaStreamWaitEvent(stream, c->be_out[(k - 1) & 1], 0));   // bs_out is in order: the last covers all
