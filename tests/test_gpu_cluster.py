@@ -251,3 +251,32 @@ def test_cluster_jitter_back_to_back(monkeypatch):
             check_result([to_host(t, "f32") for t in ts], xs, "f32", "sum", algo, n)
     finally:
         c.destroy()
+
+
+def test_cluster_random_sweep(monkeypatch):
+    """Seeded random configurations through the cluster transport — n, dtype,
+    op, whole-pack count (up to ~4 MiB per rank), channel count — each checked
+    against the oracle; ring and tree alternate, back to back per comm."""
+    rng = np.random.default_rng(2026)
+    for n in (2, 3, 4, 6, 7, 8):
+        c = _comm(n, monkeypatch)
+        try:
+            pending = []
+            for it in range(12):
+                dtype = synth.DTYPES[int(rng.integers(len(synth.DTYPES)))]
+                op = ("sum", "max", "min")[int(rng.integers(3))]
+                per = 16 // ES[dtype]
+                count = per * int(rng.integers(1, (4 << 20) // 16))
+                algo = ("ring", "tree")[it % 2]
+                nch = int(rng.integers(1, 33))
+                xs = synth.gen_ranks(dtype, count, n, cfg=900 + it, dist=default_dist(dtype))
+                ts = [to_device(x, dtype) for x in xs]
+                c.allreduce_forced(ts, algo, "simple", nch, op=op)
+                assert c.transport() == "cluster"
+                pending.append((xs, ts, dtype, op, algo))
+            torch.cuda.synchronize()
+            c.check()
+            for xs, ts, dtype, op, algo in pending:
+                check_result([to_host(t, dtype) for t in ts], xs, dtype, op, algo, n)
+        finally:
+            c.destroy()
