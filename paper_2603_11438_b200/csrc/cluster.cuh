@@ -877,34 +877,54 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
 // Full barriers are armed by the senders' warps (remote arrive.expect_tx with
 // the bytes each warp sent), credits are returned by each consuming warp: the
 // up and down groups have kTrGroup warps each, so every count is kTrGroup.
-// (Measured and not adopted: a double binary tree — half of each channel through
-// the tree with positions shifted by ceil(n/2), whose interior nodes are this
-// tree's leaves, so no SM moves more than 2 tiles per tile instead of 3.
-// Interleaved tile by tile in one pipeline every tile chains through both
-// trees: 128 MiB 5990 us; as two concurrent pipelines on disjoint warps and
-// half the shared memory each: 1184-2774 us vs 1107 us for this tree;
-// profiles/r02dd_*, r02ee_*.)
-#ifndef POLAR_TR_WIRE
-#define POLAR_TR_WIRE 1024        // 16-B wire words per stage (16 KiB)
-#endif
-#ifndef POLAR_TR_UP
-#define POLAR_TR_UP 4             // stages per child up inbox
-#endif
-#ifndef POLAR_TR_DN
-#define POLAR_TR_DN 3             // stages of the down inbox
-#endif
-#ifndef POLAR_TR_OWN
-#define POLAR_TR_OWN 2            // own-input stages
-#endif
+// (With the down phase on DSMEM a double binary tree was slower — interleaved
+// tile by tile in one pipeline every tile chains through both trees, 5990 us;
+// two concurrent pipelines 1184-2774 us vs 1107 us; profiles/r02dd_*, r02ee_*.
+// With the L2 down phase it wins: POLAR_TR_DBT2 below.)
 #ifndef POLAR_TR_L2DN
 #define POLAR_TR_L2DN 1
 #endif
-#ifndef POLAR_TR_GROUP
-#if POLAR_TR_L2DN
-#define POLAR_TR_GROUP 16         // up-group warps (128 MiB f32, HBM frac: 0.34 with 4, 0.52 with 8, 0.56 with 16, 0.54 with 24)
-#else
-#define POLAR_TR_GROUP 4          // warps per group (up, down)
+#ifndef POLAR_TR_DBT2
+#define POLAR_TR_DBT2 1
 #endif
+// Defaults per shape (8 x 128 MiB f32, fraction of the HBM copy peak):
+//   single tree, L2 down: 16 KiB tiles, up group 4 / 8 / 16 / 24 warps:
+//                         0.34 / 0.52 / 0.56 / 0.54
+//   double tree (DBT2):   8 KiB tiles, per tree 6 / 8 / 12 up warps:
+//                         0.54 / 0.65 / 0.61 (profiles/r02ee_*, r02kk_*)
+#if POLAR_TR_DBT2 && POLAR_TR_L2DN
+#define POLAR_TR_WIRE_D 512
+#define POLAR_TR_UP_D 3
+#define POLAR_TR_DN_D 4
+#define POLAR_TR_OWN_D 4
+#define POLAR_TR_GROUP_D 8
+#elif POLAR_TR_L2DN
+#define POLAR_TR_WIRE_D 1024
+#define POLAR_TR_UP_D 4
+#define POLAR_TR_DN_D 3
+#define POLAR_TR_OWN_D 2
+#define POLAR_TR_GROUP_D 16
+#else
+#define POLAR_TR_WIRE_D 1024
+#define POLAR_TR_UP_D 4
+#define POLAR_TR_DN_D 3
+#define POLAR_TR_OWN_D 2
+#define POLAR_TR_GROUP_D 4
+#endif
+#ifndef POLAR_TR_WIRE
+#define POLAR_TR_WIRE POLAR_TR_WIRE_D   // 16-B wire words per stage
+#endif
+#ifndef POLAR_TR_UP
+#define POLAR_TR_UP POLAR_TR_UP_D       // stages per child up inbox
+#endif
+#ifndef POLAR_TR_DN
+#define POLAR_TR_DN POLAR_TR_DN_D       // down stages (pull / staging in L2 mode)
+#endif
+#ifndef POLAR_TR_OWN
+#define POLAR_TR_OWN POLAR_TR_OWN_D     // own-input stages
+#endif
+#ifndef POLAR_TR_GROUP
+#define POLAR_TR_GROUP POLAR_TR_GROUP_D // up-group warps (per tree)
 #endif
 // POLAR_TR_L2DN (the default): the down phase through L2 instead of DSMEM.  The
 // root's up group stages each result tile in shared memory; one down warp
@@ -915,14 +935,25 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
 // in turn.  DSMEM then carries only the up phase: an interior node moves 2
 // tiles in and 1 out per tile (f32) instead of 3 and 3.
 constexpr bool kTrL2 = POLAR_TR_L2DN != 0;
+// POLAR_TR_DBT2 (the default, with the L2 down phase): a double binary tree —
+// the channel's tiles cut in halves, the second half through the tree with
+// every position shifted by ceil(n/2) (its interior nodes are the first
+// tree's leaves); the two trees run concurrently on disjoint warps and shared
+// memory.  With the down phase in L2 a leaf receives nothing through DSMEM, so
+// no SM takes in more than 2 tiles per 2 tiles of the channel instead of 2 per
+// tile.  (The reduction order of the second half differs from the FIFO
+// tree's: f32 sums match it within the tree's bound, integer-valued exactly.)
+constexpr int kTrTrees = (POLAR_TR_DBT2 && POLAR_TR_L2DN) ? 2 : 1;
 constexpr unsigned kTrWire = POLAR_TR_WIRE;
 constexpr size_t kTrStage = (size_t)kTrWire * 16;
 constexpr int kTrUp = POLAR_TR_UP, kTrDn = POLAR_TR_DN, kTrOwn = POLAR_TR_OWN, kTrGroup = POLAR_TR_GROUP;
-constexpr int kTrThreads = 32 * (1 + kTrGroup + (kTrL2 ? 1 : kTrGroup));
+constexpr int kTrWarpsPerTree = 1 + kTrGroup + (kTrL2 ? 1 : kTrGroup);
+constexpr int kTrThreads = 32 * kTrWarpsPerTree * kTrTrees;
 constexpr int kTrNbar = 2 * kTrUp + kTrUp + kTrDn + 2 * kTrDn + 2 * kTrOwn + 1;
 __host__ __device__ constexpr size_t cl_tree_smem_bytes() {
-    return (size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8 + 8;
+    return ((size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8 + 16) * kTrTrees;
 }
+__host__ __device__ constexpr size_t cl_tree_bytes_per_tree() { return cl_tree_smem_bytes() / kTrTrees; }
 struct ClTreeSmem {
     uint32_t up[2], dn, own;            // inboxes (child k up, parent down), own stages
     uint32_t upfull[2], upempty;        // up inbox k landed / my up sends' credits
@@ -1067,9 +1098,12 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
     const int n = P.nranks;
     const int r = (int)cluster_rank();
     const int c = (int)blockIdx.x / n;
-    const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
-    const int pos = ((r - c) % n + n) % n;
-    auto rank_of = [&](int q) { return (q + c) % n; };
+    const int lane = (int)(threadIdx.x & 31);
+    const int tree = (int)(threadIdx.x >> 5) / kTrWarpsPerTree;            // (POLAR_TR_DBT2: 0 or 1)
+    const int warp = (int)(threadIdx.x >> 5) % kTrWarpsPerTree;            // role within the tree
+    const int shift = tree * ((n + 1) / 2);
+    const int pos = ((r - c + shift) % n + n) % n;
+    auto rank_of = [&](int q) { return ((q - shift + c) % n + n) % n; };
     const bool root = pos == 0;
     const int parent = root ? -1 : rank_of((pos - 1) / 2);
     const int my_idx = root ? 0 : (pos - 1) % 2;
@@ -1080,8 +1114,9 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
     const bool tel = P.tel != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     const unsigned long long tel_t0 = tel ? globaltimer() : 0;
     extern __shared__ __align__(128) unsigned char smem[];
-    const ClTreeSmem S = cl_tree_smem(smem_u32(smem));
-    if (threadIdx.x == 0) {
+    const ClTreeSmem S = cl_tree_smem(smem_u32(smem) + (uint32_t)(tree * cl_tree_bytes_per_tree()));
+    const uint32_t fin0 = cl_tree_smem(smem_u32(smem)).fin;   // the CTA's rendezvous (tree 0's)
+    if (warp == 0 && lane == 0) {
         for (int x = 0; x < kTrUp; ++x) {
             mbar_init_u32(S.upfull[0] + 8u * x, kTrGroup);
             mbar_init_u32(S.upfull[1] + 8u * x, kTrGroup);
@@ -1101,12 +1136,19 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
         if (kTrL2)
             asm volatile("st.shared.u32 [%0], 0;\n\tst.shared.u32 [%1], %2;" ::"r"(S.cnt), "r"(S.stok), "n"(kTrDn)
                          : "memory");
-        mbar_init_u32(S.fin, (uint32_t)(n - 1));
+        if (tree == 0) mbar_init_u32(S.fin, (uint32_t)(n - 1));
         mbar_fence_init();
     }
     cluster_sync_all();
     unsigned long long ca, cb;
     split_range(0, npacks<ES>(P), P.nch, c, ca, cb);
+    if (kTrTrees > 1) {
+        // tree t takes half of the channel's tiles
+        const unsigned long long tiles = (cb - ca + TP - 1) / TP;
+        const unsigned long long mid = ca + (tiles + 1) / 2 * TP < cb ? ca + (tiles + 1) / 2 * TP : cb;
+        if (tree == 0) cb = mid;
+        else ca = mid;
+    }
     uint4* mine = reinterpret_cast<uint4*>(P.bufs[r]);
     // remote addresses: my up inbox slot at the parent, the children's down inboxes
     const uint32_t par_up = root ? 0u : cl_map(S.up[my_idx], (uint32_t)parent);
@@ -1259,7 +1301,7 @@ __global__ void __launch_bounds__(kTrThreads, 1) tree_cluster_kernel(Params P) {
             if (nchild) dn.next(kTrDn);
         }
     }
-    cl_rendezvous(P, S.fin, r, n);
+    cl_rendezvous(P, fin0, r, n);
     if (tel) {
         volatile TelEntry* e = P.tel + (P.seq % kTelRing);
         e->t0 = tel_t0;

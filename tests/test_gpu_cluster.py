@@ -64,29 +64,34 @@ def test_cluster_matrix(algo, n, monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_cluster_tree_matches_fifo_bitwise(dtype, monkeypatch):
-    """The tree's reduction order (own (op) child0 (op) child1, root = rank c
-    mod n) does not depend on tiling: for the same channel count the cluster
-    tree and the FIFO tree give the same bits (f32 / bf16 sums of real data),
-    at sizes below and above the tree's default cluster bound."""
+def test_cluster_tree_vs_fifo_tree(dtype, monkeypatch):
+    """The cluster tree (a double binary tree: the second half of each channel
+    through the tree with positions shifted by ceil(n/2)) against the FIFO
+    tree: every element is reduced up one binary tree in both, so integer-valued
+    inputs give identical results, and real data stays within the tree's bound
+    (R2 / R3); sizes from one tile to many, channel counts 1..15."""
     n = 8
-    a = _comm(n, monkeypatch, cluster=True, POLAR_CLUSTER_TREE_MAX=1 << 40)
+    a = _comm(n, monkeypatch, cluster=True)
     b = _comm(n, monkeypatch, cluster=False)
     try:
         for count, nch in ((4096, 1), (123_456, 5), (2_000_000, 15), (9_000_000, 15)):
             count = _aligned(count, dtype)
-            xs = synth.gen_ranks(dtype, count, n, cfg=33, dist=default_dist(dtype))
-            ta = [to_device(x, dtype) for x in xs]
-            tb = [to_device(x, dtype) for x in xs]
-            a.allreduce_forced(ta, "tree", "simple", nch)
-            b.allreduce_forced(tb, "tree", "simple", nch)
-            assert a.transport() == "cluster" and b.transport() == "peer"
-            assert a.launched_channels() == b.launched_channels() == nch
-            torch.cuda.synchronize()
-            a.check()
-            for x, y in zip(ta, tb):
-                assert np.array_equal(to_host(x, dtype), to_host(y, dtype)), count
-            check_result([to_host(t, dtype) for t in ta], xs, dtype, "sum", "tree", n)
+            for dist in ("ints", default_dist(dtype)):
+                xs = synth.gen_ranks(dtype, count, n, cfg=33, dist=dist)
+                ta = [to_device(x, dtype) for x in xs]
+                tb = [to_device(x, dtype) for x in xs]
+                a.allreduce_forced(ta, "tree", "simple", nch)
+                b.allreduce_forced(tb, "tree", "simple", nch)
+                assert a.transport() == "cluster" and b.transport() == "peer"
+                assert a.launched_channels() == b.launched_channels() == nch
+                torch.cuda.synchronize()
+                a.check()
+                got = [to_host(t, dtype) for t in ta]
+                check_result(got, xs, dtype, "sum", "tree", n)
+                if dist == "ints":
+                    fifo = to_host(tb[0], dtype)
+                    for g in got:
+                        assert np.array_equal(g, fifo), count
     finally:
         a.destroy()
         b.destroy()
