@@ -283,9 +283,17 @@ __device__ __forceinline__ void cluster_sync_all() {
 // Final rendezvous: no CTA leaves while a peer may still touch its shared memory
 // (the successor's last credits land on my `empty` barriers after my loop).
 // Thread 0 of each CTA arrives on every peer's `fin` and waits for its own.
+// The fence matters: every warp's remote operations (credits on a peer's
+// barriers, published counts, st.async) precede the __syncthreads, and the
+// cluster-scope fence orders them before the fin arrives — a relaxed fin
+// arrive could otherwise overtake, say, the signal warp's last credit, the
+// peer could leave, and the late credit would land in the shared memory of
+// the next kernel's CTA on that SM (compute-sanitizer memcheck caught the
+// resulting launch failure in a back-to-back sequence).
 __device__ __forceinline__ void cl_rendezvous(const Params& P, uint32_t fin, int r, int n) {
     __syncthreads();
     if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
         for (int p = 0; p < n; ++p)
             if (p != r) cl_arrive_remote(cl_map(fin, (uint32_t)p));
         if (!cl_try_wait(fin, 0)) cl_wait_slow(fin, 0, P.timeout_ns, P.err, 0);
