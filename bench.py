@@ -329,7 +329,7 @@ def run_polar(args):
             dist.all_gather_object(out, b)
             return out
 
-        comm = L.Comm.init(ws, rank, local, allgather)
+        comm = L.Comm.init(ws, rank, local, L.torch_allgather(dist, ws))
         n = ws
         # LL128's premise over this transport (a real comm refuses LL128 until it passed)
         t0 = time.perf_counter()
@@ -438,6 +438,33 @@ def run_polar(args):
                  "ratio_vs_registered": round(tu / t_step, 4),
                  "path": "torch tensor, not registered: two-shot via the bounce region, copy-in / kernel / copy-out "
                          "pipelined over 2 x POLAR_BOUNCE/2 halves"}
+        # the same tensor with auto-registration (polar_comm_autoreg): one IPC-handle
+        # all-gather per call on the host, zero-copy on the device
+        comm.autoreg(True, 1 << 20)
+        for _ in range(args.warmup):
+            ustep()
+        torch.cuda.synchronize()
+        barrier()
+        ta = max_over_ranks(_time_calls(ustep, uk, stream))
+        comm.check()
+        # one more auto-registered call on the re-filled tensor: bitwise equal to
+        # the registered buffer's checked result (same inputs, same kernel), on every rank
+        plain.copy_(torch.from_numpy(host_inputs[0]))
+        torch.cuda.synchronize()
+        barrier()
+        ustep()
+        torch.cuda.synchronize()
+        comm.check()
+        ars = comm.autoreg_stats()
+        comm.autoreg(False)
+        same = bool(torch.equal(plain.view(torch.int32), bufs[0].view(torch.int32)))
+        got = allgather(hashlib.sha1(plain.cpu().numpy().tobytes()).hexdigest())
+        unreg["autoreg"] = {"busbw_gbs": round(busbw(S_BYTES, n, ta), 2), "us": round(ta * 1e6, 1), "steps": uk,
+                            "ratio_vs_registered": round(ta / t_step, 4), "stats": ars,
+                            "parity": {"equal_to_checked_registered_result": same,
+                                       "ranks_identical": len(set(got)) == 1},
+                            "path": "the same tensor, auto-registered: per call one host all-gather of "
+                                    "{IPC handle, buffer id, offset}, peer allocations opened once, zero-copy two-shot"}
         del plain
 
     # roofline of the (only) kernel of the step: the dispatched allreduce kernel

@@ -259,6 +259,35 @@ polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes);
  * uses).  POLAR_OK also when `buf` is not (or no longer) registered. */
 polar_status polar_deregister(polar_comm_t comm, void* buf);
 
+/* Auto-registration (collective; every rank passes the same values, else
+ * POLAR_EINVAL and nothing changes).  With enable != 0, a real-comm AllReduce
+ * on an UNREGISTERED buffer whose decision is two-shot Simple and whose message
+ * is >= min_bytes exchanges, through the comm's all-gather callback, each rank's
+ * {CUDA-IPC handle of the allocation holding the buffer, its buffer id, the
+ * buffer's offset}; each rank maps the peers' allocations (opened once per
+ * allocation and cached, at most 32 per peer, least recently used closed after a
+ * device synchronise) and the call runs zero-copy, as on a registration.  So the
+ * call costs one small host all-gather instead of the bounce region's local
+ * copies (north_star's allreduce(buf, ...) on caller memory).
+ * Offsets may differ between ranks.  If any rank's buffer is not
+ * IPC-exportable (cuMem/VMM memory, e.g. expandable segments) every rank takes
+ * the bounce path for that call — the choice depends on the gathered records
+ * only, so ranks agree.  A peer allocation freed and re-allocated is detected
+ * by its buffer id (the stale mapping is closed and the new one opened).  The
+ * all-gather callback is invoked from inside polar_allreduce (also while a
+ * stream is being captured into a CUDA graph: the graph keeps the pointers of
+ * capture time).  Virtual comms accept and ignore it.  Default: off. */
+polar_status polar_comm_autoreg(polar_comm_t comm, int enable, size_t min_bytes);
+
+typedef struct {
+    uint64_t exchanges;  /* auto-registration exchanges (one host all-gather each) */
+    uint64_t zero_copy;  /* ... of which ran zero-copy */
+    uint64_t bounced;    /* ... of which took the bounce path (a rank's buffer not exportable) */
+    uint64_t opens;      /* peer allocations opened (cudaIpcOpenMemHandle) */
+    uint64_t evictions;  /* auto-opened mappings closed (cache bound, stale allocation) */
+} polar_autoreg_stats;
+polar_status polar_comm_autoreg_stats(polar_comm_t comm, polar_autoreg_stats* out);
+
 /* ----------------------------------------------------------------- AllReduce */
 
 /* In-place AllReduce of `count` elements at device pointer `buf` (real comm,

@@ -114,8 +114,12 @@ struct polar_comm_s {
     uint32_t reg_seq = 0;                // registrations made (collective, so equal on every rank)
     uint64_t stale_regs = 0;             // user registrations dropped because their allocation was freed
     std::vector<char*> ipc_mapped;       // to close at destroy
-    struct Opened { int peer; cudaIpcMemHandle_t h; char* base; };
-    std::vector<Opened> opened;          // IPC handles already opened (one open per allocation)
+    // IPC handles already opened (one open per allocation).  peer_bid: the
+    // peer's CU_POINTER_ATTRIBUTE_BUFFER_ID of that allocation when known (the
+    // auto-registration exchange sends it; 0 from polar_register); last_use: the
+    // auto-registration call that last used the mapping (0: never)
+    struct Opened { int peer; cudaIpcMemHandle_t h; char* base; unsigned long long peer_bid; uint64_t last_use; };
+    std::vector<Opened> opened;
     std::vector<char*> virt_allocs;      // polar_mem_alloc on virtual comms
     int* err_host = nullptr;
     int* err_dev = nullptr;
@@ -166,6 +170,14 @@ struct polar_comm_s {
     bool cluster = false;
     int cl_max_ch[5] = {};               // per algorithm id
     size_t cl_tree_max = ~(size_t)0;     // cluster tree up to this many bytes per rank (POLAR_CLUSTER_TREE_MAX)
+    // auto-registration (polar_comm_autoreg): unregistered two-shot calls of at
+    // least autoreg_min bytes exchange their buffers' IPC handles (one host
+    // all-gather per call) and run zero-copy; the handles this rank exported,
+    // by allocation (CU_POINTER_ATTRIBUTE_BUFFER_ID)
+    size_t autoreg_min = ~(size_t)0;     // off
+    struct Exported { unsigned long long bid; char* base; cudaIpcMemHandle_t h; };
+    std::vector<Exported> exported;
+    polar_autoreg_stats ar{};
     std::mutex mu;
 };
 
@@ -542,24 +554,34 @@ void destroy_comm(polar_comm_s* c, bool collective) {
     delete c;
 }
 
-// Exchange IPC handles of `base` (allocation start) + offset; fill peer[] pointers.
-polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks], char* peer_base[kMaxRanks] = nullptr) {
-    struct Msg { cudaIpcMemHandle_t h; unsigned long long off; int pid_ok; };
-    CUdeviceptr base = 0;
-    size_t sz = 0;
-    // cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link)
+// The allocation containing p: cuMemGetAddressRange through the runtime's
+// driver entry point (no -lcuda link).  false if unknown.
+bool alloc_range(const void* p, char** base, size_t* bytes) {
     static CUresult (*getrange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
     if (!getrange) {
         cudaDriverEntryPointQueryResult q;
         void* fp = nullptr;
         if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess || !fp)
-            return POLAR_ECUDA;
+            return false;
         getrange = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fp);
     }
-    if (getrange(&base, &sz, (CUdeviceptr)ptr) != CUDA_SUCCESS) return POLAR_EINVAL;
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (getrange(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+    *base = reinterpret_cast<char*>(b);
+    *bytes = sz;
+    return true;
+}
+
+// Exchange IPC handles of `base` (allocation start) + offset; fill peer[] pointers.
+polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks], char* peer_base[kMaxRanks] = nullptr) {
+    struct Msg { cudaIpcMemHandle_t h; unsigned long long off; int pid_ok; };
+    char* base = nullptr;
+    size_t sz = 0;
+    if (!alloc_range(ptr, &base, &sz)) return POLAR_EINVAL;
     Msg mine{};
     CU_TRY(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)));
-    mine.off = (unsigned long long)(ptr - reinterpret_cast<char*>(base));
+    mine.off = (unsigned long long)(ptr - base);
     mine.pid_ok = 1;
     std::vector<Msg> all(c->nranks);
     if (c->ag(&mine, all.data(), sizeof(Msg), c->user) != 0) return POLAR_ESTATE;
@@ -577,11 +599,150 @@ polar_status exchange_and_map(polar_comm_s* c, char* ptr, char* peer[kMaxRanks],
             if (e != cudaSuccess) { (void)cudaGetLastError(); return POLAR_ECUDA; }
             base_p = reinterpret_cast<char*>(m);
             c->ipc_mapped.push_back(base_p);
-            c->opened.push_back({p, all[p].h, base_p});
+            c->opened.push_back({p, all[p].h, base_p, 0ull, 0});
         }
         peer[p] = base_p + all[p].off;
         if (peer_base) peer_base[p] = base_p;
     }
+    return POLAR_OK;
+}
+
+// ------------------------------------------------------- auto-registration
+// polar_comm_autoreg (DESIGN.md §8 "Unregistered buffers: auto-registration").
+// An unregistered two-shot call of at least autoreg_min bytes: every rank sends
+// {IPC handle of the allocation holding its buffer, that allocation's buffer
+// id, the buffer's offset in it, the call's bytes, ok}; every rank maps the
+// peers' allocations (cached per (peer, handle, buffer id): the first call on
+// an allocation opens it, later calls only exchange) and addresses peer p's
+// buffer as its mapping + offset_p, so offsets may differ between ranks.  Zero
+// copy or bounce is decided from the gathered records alone, hence the same on
+// every rank; a rank whose buffer is not IPC-exportable (cuMem / VMM memory)
+// sends ok = 0 and every rank bounces.  The path hash (buffer ids and offsets
+// of all ranks) goes into the decision tag.
+constexpr size_t kAutoExported = 64;   // exported handles remembered (per comm)
+constexpr size_t kAutoMapped = 32;     // auto-opened peer mappings kept per peer
+constexpr uint64_t kPathAuto = 0xA0705E6ull;
+
+struct AutoMsg {
+    cudaIpcMemHandle_t h;
+    unsigned long long bid, off, bytes;
+    uint32_t ok, pad;
+};
+
+// close mapping k of c->opened (no registration uses it); the device is
+// synchronised first: a kernel of mine still in flight may address it
+void close_opened(polar_comm_s* c, size_t k) {
+    cudaDeviceSynchronize();
+    char* b = c->opened[k].base;
+    cudaIpcCloseMemHandle(b);
+    c->opened.erase(c->opened.begin() + (long)k);
+    for (size_t m = 0; m < c->ipc_mapped.size(); ++m)
+        if (c->ipc_mapped[m] == b) {
+            c->ipc_mapped.erase(c->ipc_mapped.begin() + (long)m);
+            break;
+        }
+    c->ar.evictions++;
+}
+
+bool used_by_registration(const polar_comm_s* c, int p, const char* b) {
+    for (const auto& r : c->regs)
+        if (r.peer_base[p] == b) return true;
+    return false;
+}
+
+// *zc = true: ptrs[] hold every rank's buffer as addressable here, *path the
+// tag component; *zc = false: bounce (every rank agrees).  ESTATE if the
+// all-gather fails, ECUDA if a peer's handle cannot be opened.
+polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, char* ptrs[kMaxRanks], uint64_t* path, bool* zc) {
+    *zc = false;
+    AutoMsg m{};
+    m.bytes = bytes;
+    char* base = nullptr;
+    size_t sz = 0;
+    const unsigned long long bid = buffer_id_of(mine);
+    if (bid && alloc_range(mine, &base, &sz) && mine + bytes <= base + sz) {
+        int e = -1;
+        for (size_t i = 0; i < c->exported.size(); ++i)
+            if (c->exported[i].bid == bid && c->exported[i].base == base) e = (int)i;
+        if (e < 0) {
+            polar_comm_s::Exported x{bid, base, {}};
+            if (cudaIpcGetMemHandle(&x.h, base) == cudaSuccess) {
+                if (c->exported.size() >= kAutoExported) c->exported.erase(c->exported.begin());
+                c->exported.push_back(x);
+                e = (int)c->exported.size() - 1;
+            } else {
+                (void)cudaGetLastError();
+            }
+        }
+        if (e >= 0) {
+            m.h = c->exported[(size_t)e].h;
+            m.bid = bid;
+            m.off = (unsigned long long)(mine - base);
+            m.ok = 1;
+        }
+    }
+    std::vector<AutoMsg> all(c->nranks);
+    c->ar.exchanges++;
+    if (c->ag(&m, all.data(), sizeof(AutoMsg), c->user) != 0) return POLAR_ESTATE;
+    bool ok = true;
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (int p = 0; p < c->nranks; ++p) {
+        ok = ok && all[p].ok && all[p].bytes == bytes;
+        h = (h ^ all[p].bid) * 0x100000001B3ull;
+        h = (h ^ all[p].off) * 0x100000001B3ull;
+    }
+    if (!ok) {
+        c->ar.bounced++;
+        return POLAR_OK;
+    }
+    const uint64_t use = c->ar.exchanges;
+    for (int p = 0; p < c->nranks; ++p) {
+        if (p == c->rank0) {
+            ptrs[p] = mine;
+            continue;
+        }
+        long k = -1;
+        for (size_t i = 0; i < c->opened.size(); ++i)
+            if (c->opened[i].peer == p && std::memcmp(&c->opened[i].h, &all[p].h, sizeof(cudaIpcMemHandle_t)) == 0) {
+                k = (long)i;
+                break;
+            }
+        if (k >= 0 && c->opened[(size_t)k].peer_bid && c->opened[(size_t)k].peer_bid != all[p].bid) {
+            // the same handle for another allocation of the peer (freed and
+            // re-allocated): the mapping is stale
+            if (used_by_registration(c, p, c->opened[(size_t)k].base)) return POLAR_ESTATE;
+            close_opened(c, (size_t)k);
+            k = -1;
+        }
+        if (k < 0) {
+            // bound the auto-opened mappings of this peer: drop the least recently used
+            size_t nmap = 0, lru = 0;
+            uint64_t oldest = ~0ull;
+            for (size_t i = 0; i < c->opened.size(); ++i) {
+                const auto& o = c->opened[i];
+                if (o.peer != p || o.last_use == 0 || used_by_registration(c, p, o.base)) continue;
+                ++nmap;
+                if (o.last_use < oldest && o.last_use != use) { oldest = o.last_use; lru = i; }
+            }
+            if (nmap >= kAutoMapped && oldest != ~0ull) close_opened(c, lru);
+            void* mp = nullptr;
+            if (cudaIpcOpenMemHandle(&mp, all[p].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                (void)cudaGetLastError();
+                return POLAR_ECUDA;
+            }
+            c->ipc_mapped.push_back(reinterpret_cast<char*>(mp));
+            c->opened.push_back({p, all[p].h, reinterpret_cast<char*>(mp), all[p].bid, use});
+            c->ar.opens++;
+            k = (long)c->opened.size() - 1;
+        }
+        auto& o = c->opened[(size_t)k];
+        o.peer_bid = all[p].bid;
+        o.last_use = use;
+        ptrs[p] = o.base + all[p].off;
+    }
+    *path = h;
+    *zc = true;
+    c->ar.zero_copy++;
     return POLAR_OK;
 }
 
@@ -804,6 +965,25 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0,
                               ((uint64_t)(reg->id + 1) << 40) ^ (uint64_t)off);
         return launch_kernel(c, fn, P, grid, stream, smem);
+    }
+    if (bytes >= c->autoreg_min && c->ag) {
+        // auto-registration: one handle exchange, then zero-copy like a registration
+        char* ptrs[kMaxRanks] = {};
+        uint64_t path = 0;
+        bool zc = false;
+        st = autoreg_map(c, mine, bytes, ptrs, &path, &zc);
+        if (st != POLAR_OK) return st;
+        if (zc) {
+            bool vec = true;
+            for (int p = 0; p < c->nranks; ++p) {
+                P.bufs[p] = ptrs[p];
+                vec = vec && (reinterpret_cast<uintptr_t>(ptrs[p]) % 16 == 0);
+            }
+            P.vec = vec;
+            P.count = count;
+            P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0, kPathAuto ^ path);
+            return launch_kernel(c, fn, P, grid, stream, smem);
+        }
     }
     // Unregistered buffer: its peers cannot address it, so it travels through
     // the symmetric bounce region, split in two halves that alternate by chunk.
@@ -1184,6 +1364,29 @@ polar_status polar_deregister(polar_comm_t comm, void* buf) {
         }
     // (not registered here, or already dropped as stale: still collective, still OK)
     return st;
+}
+
+polar_status polar_comm_autoreg(polar_comm_t comm, int enable, size_t min_bytes) {
+    if (!comm) return POLAR_EINVAL;
+    const size_t want = enable ? min_bytes : ~(size_t)0;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    if (!comm->is_virtual && comm->nranks > 1) {
+        // collective: every rank must exchange on the same calls
+        if (!comm->ag) return POLAR_EINVAL;
+        unsigned long long mine = want, all[kMaxRanks];
+        if (comm->ag(&mine, all, sizeof(mine), comm->user) != 0) return POLAR_ESTATE;
+        for (int p = 0; p < comm->nranks; ++p)
+            if (all[p] != mine) return POLAR_EINVAL;
+    }
+    comm->autoreg_min = want;
+    return POLAR_OK;
+}
+
+polar_status polar_comm_autoreg_stats(polar_comm_t comm, polar_autoreg_stats* out) {
+    if (!comm || !out) return POLAR_EINVAL;
+    std::lock_guard<std::mutex> lk(comm->mu);
+    *out = comm->ar;
+    return POLAR_OK;
 }
 
 polar_status polar_allreduce(polar_comm_t comm, void* buf, size_t count, polar_dtype dtype, polar_op op,

@@ -92,6 +92,11 @@ class AdaptiveState(C.Structure):
                 ("samples", C.c_uint64), ("last_mean_ns", C.c_double)]
 
 
+class AutoregStats(C.Structure):
+    _fields_ = [("exchanges", C.c_uint64), ("zero_copy", C.c_uint64), ("bounced", C.c_uint64),
+                ("opens", C.c_uint64), ("evictions", C.c_uint64)]
+
+
 AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 _P = C.c_void_p
@@ -114,6 +119,8 @@ _sigs = {
     "polar_mem_free": (C.c_int, [_P, _P]),
     "polar_register": (C.c_int, [_P, _P, C.c_size_t]),
     "polar_deregister": (C.c_int, [_P, _P]),
+    "polar_comm_autoreg": (C.c_int, [_P, C.c_int, C.c_size_t]),
+    "polar_comm_autoreg_stats": (C.c_int, [_P, C.POINTER(AutoregStats)]),
     "polar_allreduce": (C.c_int, [_P, _P, C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_allreduce_v": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, _P]),
     "polar_allreduce_forced": (C.c_int, [_P, C.POINTER(_P), C.c_size_t, C.c_int, C.c_int, C.POINTER(Decision), _P]),
@@ -275,6 +282,23 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
 
+def torch_allgather(dist, world_size: int, group=None):
+    """allgather(bytes) -> list[bytes] over a torch.distributed (CPU / gloo)
+    group, for Comm.init: every payload of one call has the same size (the C
+    ABI's fixed-size records), so it moves as one uint8 tensor per rank without
+    pickling (all_gather_object costs ~10x more per call — it matters for
+    polar_comm_autoreg, which all-gathers once per call)."""
+    import torch
+
+    def ag(b: bytes):
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(world_size)]
+        dist.all_gather(out, t, group=group)
+        return [o.numpy().tobytes() for o in out]
+
+    return ag
+
+
 def _make_ag(allgather):
     """Wrap allgather(bytes) -> list[bytes] as the C callback polar_allgather_fn."""
 
@@ -359,6 +383,16 @@ class Comm:
         """Collective: drop the registration starting at this tensor's (or raw pointer's) address."""
         ptr = tensor_or_ptr if isinstance(tensor_or_ptr, int) else tensor_or_ptr.data_ptr()
         _check(lib.polar_deregister(self.h, C.c_void_p(ptr)), "polar_deregister")
+
+    def autoreg(self, enable: bool = True, min_bytes: int = 0):
+        """Collective: unregistered two-shot calls of >= min_bytes exchange IPC
+        handles and run zero-copy (polar_comm_autoreg)."""
+        _check(lib.polar_comm_autoreg(self.h, 1 if enable else 0, int(min_bytes)), "polar_comm_autoreg")
+
+    def autoreg_stats(self) -> dict:
+        s = AutoregStats()
+        _check(lib.polar_comm_autoreg_stats(self.h, C.byref(s)), "polar_comm_autoreg_stats")
+        return {k: int(getattr(s, k)) for k, _ in AutoregStats._fields_}
 
     def _list(self, tensors, what, cuda=True):
         """nlocal tensors, each a contiguous CUDA tensor, all of one dtype and numel:

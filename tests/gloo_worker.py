@@ -36,6 +36,8 @@ def main():
         os.environ["POLAR_OS_CHUNK"] = str(2 << 20)   # this rank's scratch layout differs
     rep["bootstrap"] = L.STATUS_NAMES[L.bootstrap_check(ws, rank, allgather)]
     if mode == "consistency":
+        # the same check through the pickle-free byte all-gather (polar.torch_allgather)
+        rep["bootstrap_tensor_ag"] = L.STATUS_NAMES[L.bootstrap_check(ws, rank, L.torch_allgather(dist, ws))]
         sizes = [1 << k for k in range(3, 31)] + [(1 << k) + 1 for k in range(3, 31)]
         tables = [[], [(0, 0, 32768, L.TREE, L.SIMPLE, 4), (0, 0, 2**64 - 1, L.RING, L.SIMPLE, 4)],
                   [(0, ws, 1 << 20, L.ONESHOT, L.LL, 2), (0, 0, 2**64 - 1, L.UNSET, L.UNSET, 64)]]

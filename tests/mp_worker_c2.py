@@ -47,7 +47,7 @@ def main():
         dist.all_gather_object(o, b)
         return o
 
-    comm = L.Comm.init(ws, rank, dev, allgather)
+    comm = L.Comm.init(ws, rank, dev, L.torch_allgather(dist, ws))
     results = []
     rng = np.random.default_rng(77)
     windows = [(0, 4096), (COUNT - 4099, COUNT)] + [(int(s), int(s) + 2048)
@@ -147,6 +147,74 @@ def main():
     torch.cuda.synchronize()
     comm.check()
     check("c2/deregistered", reg2, True)
+    # 8. auto-registration (polar_comm_autoreg): unregistered tensors run zero-copy
+    #    after one IPC-handle exchange per call; offsets differ between ranks
+    try:
+        comm.autoreg(rank == 0, 1 << 20)      # ranks disagree: refused on every rank
+        mism = "accepted"
+    except L.PolarError as ex:
+        mism = ex.name
+    results.append({"tag": "autoreg/mismatch-refused", "rank": rank, "ok": mism == "einval", "identical": True})
+    comm.autoreg(True, 1 << 20)
+    s0 = comm.autoreg_stats()
+    big = torch.empty(COUNT + 4096, dtype=torch.float32, device="cuda")
+    v1 = big[1024 * rank:1024 * rank + COUNT]            # 16-B aligned, rank-dependent offset
+    v1.copy_(torch.from_numpy(x_mine))
+    ar(v1)
+    torch.cuda.synchronize()
+    comm.check()
+    check("autoreg/first", v1, True)
+    s1 = comm.autoreg_stats()
+    v1.copy_(torch.from_numpy(x_mine))
+    ar(v1)                                               # the same allocation: no new open
+    v2 = torch.from_numpy(x_mine).cuda()
+    ar(v2)                                               # back to back, another allocation
+    torch.cuda.synchronize()
+    comm.check()
+    check("autoreg/again", v1, True)
+    check("autoreg/b2b-other", v2, True)
+    s2 = comm.autoreg_stats()
+    results.append({"tag": "autoreg/stats", "rank": rank, "identical": True,
+                    "ok": (s1["zero_copy"] - s0["zero_copy"] == 1 and s1["opens"] - s0["opens"] == ws - 1 and
+                           s2["zero_copy"] - s1["zero_copy"] == 2 and s2["opens"] - s1["opens"] == ws - 1),
+                    "stats": [s0, s1, s2]})
+    # unaligned, rank-dependent offsets (4-B aligned only: the kernel's scalar path)
+    v3 = big[1 + rank:1 + rank + COUNT]
+    v3.copy_(torch.from_numpy(x_mine))
+    ar(v3)
+    torch.cuda.synchronize()
+    comm.check()
+    check("autoreg/unaligned", v3, True)
+    # a freed and re-allocated buffer (the peers' old mappings are stale)
+    del v1, v2, v3, big
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    v4 = torch.from_numpy(x_mine).cuda()
+    ar(v4)
+    torch.cuda.synchronize()
+    comm.check()
+    check("autoreg/after-free", v4, True)
+    # CUDA-graph capture: the exchange runs at capture time, replays reuse the pointers
+    g = torch.cuda.CUDAGraph()
+    gs = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=gs):
+        st = L.lib.polar_allreduce(comm.h, L.C.c_void_p(v4.data_ptr()), COUNT, L.FLOAT32, L.SUM,
+                                   L.C.c_void_p(gs.cuda_stream))
+    ok_cap = st == L.OK
+    for rep in range(2):
+        v4.copy_(torch.from_numpy(x_mine))
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        comm.check()
+        check(f"autoreg/graph-replay{rep}", v4, True)
+    results.append({"tag": "autoreg/graph-captured", "rank": rank, "ok": ok_cap, "identical": True})
+    del g
+    results.append({"tag": "autoreg/final-stats", "rank": rank, "ok": True, "identical": True,
+                    "stats": comm.autoreg_stats()})
+    comm.autoreg(False)
     # 7. ranks addressing one call differently: rank 0 registered, the others not.
     #    The entry handshake compares the decision tags (path included) and every
     #    rank latches ESTATE before any data moves: every buffer keeps its input.

@@ -56,7 +56,9 @@ def test_multiprocess_north_star_size_c2(tmp_path):
     128 MiB f32 per rank (C2's largest), 3 processes on CUDA IPC: registered
     (zero-copy two-shot) and unregistered (bounce) buffers under the default
     table, forced ring / tree Simple at 32 channels, back-to-back mixes, a
-    stale (freed) registration, deregistration, and a path mismatch that must
+    stale (freed) registration, deregistration, auto-registration (rank-dependent
+    and unaligned offsets, mapping cache, a freed allocation, CUDA-graph
+    capture, a refused mismatched configuration), and a path mismatch that must
     latch ESTATE before any data moves (tests/mp_worker_c2.py)."""
     out = tmp_path / "c2.json"
     env = dict(os.environ)
@@ -71,10 +73,14 @@ def test_multiprocess_north_star_size_c2(tmp_path):
     assert not bad, bad
     tags = {x["tag"] for x in res}
     assert {"c2/registered/policy", "c2/unregistered/policy", "c2/ring/simple/32ch", "c2/tree/simple/32ch",
-            "c2/after-free", "c2/deregistered", "path-mismatch-latched-before-data"} <= tags
+            "c2/after-free", "c2/deregistered", "path-mismatch-latched-before-data",
+            "autoreg/mismatch-refused", "autoreg/first", "autoreg/again", "autoreg/b2b-other", "autoreg/stats",
+            "autoreg/unaligned", "autoreg/after-free", "autoreg/graph-replay0", "autoreg/graph-replay1",
+            "autoreg/graph-captured"} <= tags
     dec = {x["tag"]: x["decision"] for x in res if "decision" in x}
     assert dec["c2/registered/policy"][:2] == ["twoshot", "simple"]
     assert dec["c2/unregistered/policy"][:2] == ["twoshot", "simple"]
+    assert dec["autoreg/first"][:2] == ["twoshot", "simple"]
     # R2 headroom of the f32 ring / tree results (reported, asserted <= 1 above)
     print({x["tag"]: round(x["max_err_over_bound"], 4) for x in res if x["rank"] == 0 and "max_err_over_bound" in x})
 

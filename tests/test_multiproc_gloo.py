@@ -37,7 +37,7 @@ def test_bootstrap_and_consistent_decisions(tmp_path, nranks):
     rep = _run(tmp_path, nranks, "consistency")
     assert len(rep) == nranks
     for r in rep:
-        assert r["bootstrap"] == "ok"
+        assert r["bootstrap"] == "ok" and r["bootstrap_tensor_ag"] == "ok"
         assert r["decisions_identical"] and r["gens_identical"]
         assert r["gens"] == sorted(r["gens"]) and len(set(r["gens"])) == len(r["gens"])
 
