@@ -79,6 +79,10 @@ namespace dev {
 #define POLAR_CL_OWN 4            // (3: 128 MiB f32 685 us, 4: 650 us; profiles/r02y_cluster_ring_ab.jsonl)
 #endif
 #endif
+#ifndef POLAR_CL_PF
+#define POLAR_CL_PF 0             // own tiles prefetched into L2 ahead of the TMA loads (0: off)
+#endif
+constexpr int kClPf = POLAR_CL_PF;
 constexpr int kClWarps = POLAR_CL_WARPS;
 constexpr bool kClAgL2 = POLAR_CL_AGL2 != 0;
 constexpr int kClAgP = kClAgL2 ? POLAR_CL_AGP : 0;
@@ -776,6 +780,10 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
         // warp-mates wait at the final __syncthreads diverges an aligned barrier
         // (measured: the loader starves, 32 MiB takes 65 ms).
         unsigned long long t = 0;
+        // POLAR_CL_PF > 0: L2 prefetch of the own tiles that many tiles ahead of
+        // the TMA loads (cp.async.bulk.prefetch.L2), so a stage refill hits L2
+        RingCursor pf = ring_cursor(r, n, ca, cb, SP);
+        unsigned long long npf = 0;
         const bool ok = cl_ring_walk(r, n, ca, cb, SP, TP, [&](int s, unsigned long long i0, unsigned npk) {
             if (s > n - 1) return true;
             const uint32_t x = (uint32_t)(t % kClOwn);
@@ -786,8 +794,20 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
                 mbar_expect_u32(S.ofull + 8u * x, npk * 16u);
                 bulk_load_u32(S.own + x * (uint32_t)kClStageBytes, mine + i0 * 16ull, npk * 16u, S.ofull + 8u * x);
             }
-            __syncwarp();
             ++t;
+            if constexpr (kClPf > 0) {
+                while (npf < t + (unsigned long long)kClPf) {
+                    while (!pf.done && pf.s > n - 1) ring_cursor_next(pf, r, n, cb, SP, TP);
+                    if (pf.done) break;
+                    if (lane == 0 && npf >= t)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mine + pf.i0 * 16ull),
+                                     "r"(ring_cursor_npk(pf, TP) * 16u)
+                                     : "memory");
+                    ring_cursor_next(pf, r, n, cb, SP, TP);
+                    ++npf;
+                }
+            }
+            __syncwarp();
             return true;
         });
         if (!ok && lane == 0) {
