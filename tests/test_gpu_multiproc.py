@@ -101,3 +101,27 @@ def test_tune_policy_real_ranks(tmp_path):
     assert doc["set_policy_status"] == "ok" and doc["rows"][-1][2] == 2**64 - 1
     assert doc["best_single"] and doc["ll128_probe"]["torn_lanes"] == 0
     assert set(doc["winners"]) == {"4096", "262144"}
+
+
+@pytest.mark.parametrize("vmm_rank", [None, "1"])
+def test_multiprocess_autoreg_cache_and_agreement(tmp_path, vmm_rank):
+    """polar_comm_autoreg beyond the C2 test: 40 live buffers in separate
+    allocations (the 32-per-peer mapping cache evicts, re-opens on reuse), and
+    one rank allocating from VMM memory (expandable segments: not
+    IPC-exportable) so that every rank bounces those calls; results bit-exact
+    against the oracle (tests/mp_worker_autoreg.py)."""
+    out = tmp_path / "ar.json"
+    env = dict(os.environ)
+    env.setdefault("POLAR_TIMEOUT_MS", "60000")
+    if vmm_rank is not None:
+        env["POLAR_TEST_VMM_RANK"] = vmm_rank
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "tests", "mp_worker_autoreg.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    res = json.loads(out.read_text())
+    bad = [x for x in res if not x["ok"]]
+    assert not bad, bad
+    tags = {x["tag"] for x in res}
+    assert ("cache/stats" in tags) if vmm_rank is None else ("vmm/stats" in tags)
