@@ -33,6 +33,9 @@
  *         last call of a sequence is only checked by a following launch.
  *     Ranks that pick different kernels altogether (a policy swapped on one
  *     rank only) usually wait for each other in vain: POLAR_ETIMEOUT.
+ *       * Under polar_comm_autoreg every call of >= min_bytes all-gathers the
+ *         decision tag on the host first: a disagreement returns POLAR_ESTATE
+ *         on every rank before anything is launched.
  */
 #ifndef POLAR_H
 #define POLAR_H
@@ -116,8 +119,10 @@ typedef struct {
     uint32_t flags;       /* POLAR_ROW_* bits; others must be 0     */
 } polar_policy_row;
 
-/* Host all-gather used ONLY at comm init / registration: gathers bytes_per_rank
- * from every rank into recv (rank order).  Return 0 on success. */
+/* Host all-gather (comm init, registration, collective barriers, and once per
+ * call of >= min_bytes under polar_comm_autoreg): gathers bytes_per_rank from
+ * every rank into recv (rank order); every rank passes the same size in one
+ * call.  Return 0 on success. */
 typedef int (*polar_allgather_fn)(const void* send, void* recv, size_t bytes_per_rank, void* user);
 
 typedef struct polar_comm_s* polar_comm_t;   /* opaque; owned by the library */
@@ -260,19 +265,24 @@ polar_status polar_register(polar_comm_t comm, void* buf, size_t bytes);
 polar_status polar_deregister(polar_comm_t comm, void* buf);
 
 /* Auto-registration (collective; every rank passes the same values, else
- * POLAR_EINVAL and nothing changes).  With enable != 0, a real-comm AllReduce
- * on an UNREGISTERED buffer whose decision is two-shot Simple and whose message
- * is >= min_bytes exchanges, through the comm's all-gather callback, each rank's
- * {CUDA-IPC handle of the allocation holding the buffer, its buffer id, the
- * buffer's offset}; each rank maps the peers' allocations (opened once per
+ * POLAR_EINVAL and nothing changes).  With enable != 0, every real-comm
+ * AllReduce of >= min_bytes exchanges, through the comm's all-gather callback,
+ * each rank's {decision tag, CUDA-IPC handle of the allocation holding the
+ * buffer, its buffer id, the buffer's offset} — whatever the rank's decision or
+ * registrations, so the exchanges line up on every rank; ranks that decided the
+ * call differently all return (and latch) POLAR_ESTATE here, synchronously,
+ * before anything is launched.  When the decision is two-shot Simple each rank
+ * maps the peers' allocations (opened once per
  * allocation and cached, at most 32 per peer, least recently used closed after a
  * device synchronise) and the call runs zero-copy, as on a registration.  So the
  * call costs one small host all-gather instead of the bounce region's local
  * copies (north_star's allreduce(buf, ...) on caller memory).
- * Offsets may differ between ranks.  If any rank's buffer is not
- * IPC-exportable (cuMem/VMM memory, e.g. expandable segments) every rank takes
- * the bounce path for that call — the choice depends on the gathered records
- * only, so ranks agree.  A peer allocation freed and re-allocated is detected
+ * Offsets may differ between ranks, and registrations are not consulted.  If
+ * any rank's buffer is not IPC-exportable (cuMem/VMM memory, e.g. expandable
+ * segments) every rank takes the bounce path for that call — the choice
+ * depends on the gathered records only, so ranks agree.  No mapping is closed
+ * while the caller's stream is being captured (the cache may then exceed its
+ * bound).  A peer allocation freed and re-allocated is detected
  * by its buffer id (the stale mapping is closed and the new one opened).  The
  * all-gather callback is invoked from inside polar_allreduce (also while a
  * stream is being captured into a CUDA graph: the graph keeps the pointers of
@@ -285,6 +295,7 @@ typedef struct {
     uint64_t bounced;    /* ... of which took the bounce path (a rank's buffer not exportable) */
     uint64_t opens;      /* peer allocations opened (cudaIpcOpenMemHandle) */
     uint64_t evictions;  /* auto-opened mappings closed (cache bound, stale allocation) */
+    uint64_t mismatches; /* exchanges whose ranks had decided the call differently (ESTATE) */
 } polar_autoreg_stats;
 polar_status polar_comm_autoreg_stats(polar_comm_t comm, polar_autoreg_stats* out);
 

@@ -625,7 +625,7 @@ constexpr uint64_t kPathAuto = 0xA0705E6ull;
 
 struct AutoMsg {
     cudaIpcMemHandle_t h;
-    unsigned long long bid, off, bytes;
+    unsigned long long bid, off, bytes, dtag;
     uint32_t ok, pad;
 };
 
@@ -650,13 +650,21 @@ bool used_by_registration(const polar_comm_s* c, int p, const char* b) {
     return false;
 }
 
-// *zc = true: ptrs[] hold every rank's buffer as addressable here, *path the
-// tag component; *zc = false: bounce (every rank agrees).  ESTATE if the
-// all-gather fails, ECUDA if a peer's handle cannot be opened.
-polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, char* ptrs[kMaxRanks], uint64_t* path, bool* zc) {
+// The exchange runs for every call of >= autoreg_min bytes on a real comm,
+// whatever this rank's decision or registrations: the call sequence (and so the
+// exchange count) is the same on every rank even when the ranks' policies or
+// registrations disagree, and the record carries the decision tag, so such a
+// disagreement is caught here, synchronously, on every rank (ESTATE latched,
+// nothing launched) instead of leaving one rank blocked in the all-gather.
+// map = the decision is two-shot Simple: *zc = true: ptrs[] hold every rank's
+// buffer as addressable here, *path the tag component; *zc = false: bounce
+// (every rank agrees).  ECUDA if a peer's handle cannot be opened.
+polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, uint64_t dtag, bool map, cudaStream_t stream,
+                         char* ptrs[kMaxRanks], uint64_t* path, bool* zc) {
     *zc = false;
     AutoMsg m{};
     m.bytes = bytes;
+    m.dtag = dtag;
     char* base = nullptr;
     size_t sz = 0;
     const unsigned long long bid = buffer_id_of(mine);
@@ -687,14 +695,23 @@ polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, char* ptrs[k
     bool ok = true;
     uint64_t h = 0xcbf29ce484222325ull;
     for (int p = 0; p < c->nranks; ++p) {
-        ok = ok && all[p].ok && all[p].bytes == bytes;
+        if (all[p].dtag != dtag || all[p].bytes != bytes) {
+            c->latched = POLAR_ESTATE;   // the ranks decided this call differently
+            c->ar.mismatches++;
+            return POLAR_ESTATE;
+        }
+        ok = ok && all[p].ok;
         h = (h ^ all[p].bid) * 0x100000001B3ull;
         h = (h ^ all[p].off) * 0x100000001B3ull;
     }
+    if (!map) return POLAR_OK;
     if (!ok) {
         c->ar.bounced++;
         return POLAR_OK;
     }
+    // no device synchronise (eviction) while the caller's stream is being captured
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
     const uint64_t use = c->ar.exchanges;
     for (int p = 0; p < c->nranks; ++p) {
         if (p == c->rank0) {
@@ -710,7 +727,7 @@ polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, char* ptrs[k
         if (k >= 0 && c->opened[(size_t)k].peer_bid && c->opened[(size_t)k].peer_bid != all[p].bid) {
             // the same handle for another allocation of the peer (freed and
             // re-allocated): the mapping is stale
-            if (used_by_registration(c, p, c->opened[(size_t)k].base)) return POLAR_ESTATE;
+            if (used_by_registration(c, p, c->opened[(size_t)k].base) || capturing) return POLAR_ESTATE;
             close_opened(c, (size_t)k);
             k = -1;
         }
@@ -724,7 +741,7 @@ polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, char* ptrs[k
                 ++nmap;
                 if (o.last_use < oldest && o.last_use != use) { oldest = o.last_use; lru = i; }
             }
-            if (nmap >= kAutoMapped && oldest != ~0ull) close_opened(c, lru);
+            if (nmap >= kAutoMapped && oldest != ~0ull && !capturing) close_opened(c, lru);
             void* mp = nullptr;
             if (cudaIpcOpenMemHandle(&mp, all[p].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                 (void)cudaGetLastError();
@@ -923,6 +940,16 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
     char* mine = reinterpret_cast<char*>(bufs[0]);
+    // auto-registration: one exchange per call of >= autoreg_min bytes, before
+    // any path choice (it is also the synchronous decision check)
+    const bool ar_on = bytes >= c->autoreg_min && c->ag != nullptr;
+    bool ar_zc = false;
+    char* ar_ptrs[kMaxRanks] = {};
+    uint64_t ar_path = 0;
+    if (ar_on) {
+        st = autoreg_map(c, mine, bytes, P.dtag, ts_simple, stream, ar_ptrs, &ar_path, &ar_zc);
+        if (st != POLAR_OK) return st;
+    }
     if (nvls) {
         // switch reduction over the bound region (nvls.cu): every rank copies its
         // input in, the kernel reduces through the multicast mapping, every rank
@@ -951,7 +978,21 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         return launch_kernel(c, fn, P, grid, stream, smem);
     }
     // zero-copy two-shot needs every rank's buffer mapped
-    const Registration* reg = find_reg(c, mine, bytes);
+    if (ar_zc) {
+        // auto-registered: every rank's buffer at its own offset
+        bool vec = true;
+        for (int p = 0; p < c->nranks; ++p) {
+            P.bufs[p] = ar_ptrs[p];
+            vec = vec && (reinterpret_cast<uintptr_t>(ar_ptrs[p]) % 16 == 0);
+        }
+        P.vec = vec;
+        P.count = count;
+        P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0, kPathAuto ^ ar_path);
+        return launch_kernel(c, fn, P, grid, stream, smem);
+    }
+    // (with auto-registration on and some rank's buffer not exportable, every
+    // rank bounces, registered or not: the gathered records decided it)
+    const Registration* reg = ar_on ? nullptr : find_reg(c, mine, bytes);
     if (reg) {
         const size_t off = (size_t)(mine - reg->base);
         bool vec = true;
@@ -965,25 +1006,6 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
         P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0,
                               ((uint64_t)(reg->id + 1) << 40) ^ (uint64_t)off);
         return launch_kernel(c, fn, P, grid, stream, smem);
-    }
-    if (bytes >= c->autoreg_min && c->ag) {
-        // auto-registration: one handle exchange, then zero-copy like a registration
-        char* ptrs[kMaxRanks] = {};
-        uint64_t path = 0;
-        bool zc = false;
-        st = autoreg_map(c, mine, bytes, ptrs, &path, &zc);
-        if (st != POLAR_OK) return st;
-        if (zc) {
-            bool vec = true;
-            for (int p = 0; p < c->nranks; ++p) {
-                P.bufs[p] = ptrs[p];
-                vec = vec && (reinterpret_cast<uintptr_t>(ptrs[p]) % 16 == 0);
-            }
-            P.vec = vec;
-            P.count = count;
-            P.dtag = decision_tag(0, (int)d.algo, (int)d.proto, P.nch, dtype, op, count, 0, kPathAuto ^ path);
-            return launch_kernel(c, fn, P, grid, stream, smem);
-        }
     }
     // Unregistered buffer: its peers cannot address it, so it travels through
     // the symmetric bounce region, split in two halves that alternate by chunk.

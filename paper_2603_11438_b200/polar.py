@@ -94,7 +94,7 @@ class AdaptiveState(C.Structure):
 
 class AutoregStats(C.Structure):
     _fields_ = [("exchanges", C.c_uint64), ("zero_copy", C.c_uint64), ("bounced", C.c_uint64),
-                ("opens", C.c_uint64), ("evictions", C.c_uint64)]
+                ("opens", C.c_uint64), ("evictions", C.c_uint64), ("mismatches", C.c_uint64)]
 
 
 AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)

@@ -7,7 +7,10 @@
   * agreement when one rank's buffer cannot be exported: the rank named by
     POLAR_TEST_VMM_RANK allocates with PyTorch's expandable segments (cuMem /
     VMM memory, no cudaIpcGetMemHandle), so every rank must take the bounce
-    path for those calls (the choice depends on the gathered records only).
+    path for those calls (the choice depends on the gathered records only);
+  * registrations are not consulted (rank 0 registered, the others not: one path);
+  * the exchange as a synchronous decision check: rank 0 decides ring, the
+    others two-shot — every rank returns ESTATE before anything is launched.
 
 Every result is compared bitwise with the oracle (two-shot: rank-ordered fold,
 bit-exact) on a window at each end and one in the middle.  Rank 0 writes JSON.
@@ -94,6 +97,36 @@ def main():
                         "ok": (s1["zero_copy"] == NBUF and s1["opens"] == NBUF * (ws - 1) and
                                s1["evictions"] == (NBUF - 32) * (ws - 1) and
                                s2["opens"] - s1["opens"] == 2 * (ws - 1) and s2["bounced"] == 0)})
+        # 3. registrations are not consulted under auto-registration: rank 0 has
+        #    its buffer registered, the others not — one path for all, exact
+        b3 = torch.from_numpy(inputs(3)).cuda()
+        if RANK == 0:
+            L.lib.polar_register(comm.h, L.C.c_void_p(b3.data_ptr()), b3.numel() * 4)
+        # (a registration is collective; rank 0 alone registering would block, so
+        # the others register a scratch tensor in the same call order)
+        else:
+            dummy = torch.empty(1 << 20, dtype=torch.float32, device="cuda")
+            L.lib.polar_register(comm.h, L.C.c_void_p(dummy.data_ptr()), dummy.numel() * 4)
+        ar(b3)
+        torch.cuda.synchronize()
+        comm.check()
+        check("mixed-registration/auto", b3, 3)
+        # 4. ranks that decide the call differently (rank 0 forces ring for this
+        #    size): the exchange compares the decision tags, every rank returns
+        #    ESTATE before anything is launched, every buffer keeps its input
+        b4 = torch.from_numpy(inputs(4)).cuda()
+        torch.cuda.synchronize()
+        if RANK == 0:
+            L.set_policy([(0, 0, 2**64 - 1, L.RING, L.SIMPLE, 8)])
+        st = L.lib.polar_allreduce(comm.h, L.C.c_void_p(b4.data_ptr()), COUNT, L.FLOAT32, L.SUM,
+                                   L.C.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize()
+        untouched = bool(np.array_equal(b4.cpu().numpy().view(np.uint32), inputs(4).view(np.uint32)))
+        s3 = comm.autoreg_stats()
+        results.append({"tag": "decision-mismatch/estate", "rank": RANK, "status": L.STATUS_NAMES[st],
+                        "untouched": untouched, "stats": s3,
+                        "ok": L.STATUS_NAMES[st] == "estate" and untouched and s3["mismatches"] == 1})
+        L.set_policy([])
     else:
         # 2. one rank's buffers live in VMM memory: every rank bounces, results exact
         for k in range(3):
