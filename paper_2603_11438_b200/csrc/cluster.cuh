@@ -921,9 +921,12 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
 //   double tree (DBT2):   8 KiB tiles, per tree 6 / 8 / 12 up warps:
 //                         0.54 / 0.65 / 0.61 (profiles/r02ee_*, r02kk_*)
 #if POLAR_TR_DBT2 && POLAR_TR_L2DN
+// stages per tree (8 KiB each, 14 fit per tree): up 4 / down 2 / own 4 —
+// 8 x 128 MiB f32 499 us, bf16 874 us; up 3 / down 4 / own 4 507 / 885;
+// 4/3/3 507 / 898; 5/2/2 551 / 895; 4/4/2 555 / 913 (profiles/r02pp_*)
 #define POLAR_TR_WIRE_D 512
-#define POLAR_TR_UP_D 3
-#define POLAR_TR_DN_D 4
+#define POLAR_TR_UP_D 4
+#define POLAR_TR_DN_D 2
 #define POLAR_TR_OWN_D 4
 #define POLAR_TR_GROUP_D 8
 #elif POLAR_TR_L2DN
@@ -978,10 +981,14 @@ constexpr int kTrUp = POLAR_TR_UP, kTrDn = POLAR_TR_DN, kTrOwn = POLAR_TR_OWN, k
 constexpr int kTrWarpsPerTree = 1 + kTrGroup + (kTrL2 ? 1 : kTrGroup);
 constexpr int kTrThreads = 32 * kTrWarpsPerTree * kTrTrees;
 constexpr int kTrNbar = 2 * kTrUp + kTrUp + kTrDn + 2 * kTrDn + 2 * kTrOwn + 1;
-__host__ __device__ constexpr size_t cl_tree_smem_bytes() {
-    return ((size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8 + 16) * kTrTrees;
+// one tree's shared memory, padded to 128 B so that the second tree's stages
+// stay 128-B aligned (bulk copies and 16-B st.async need >= 16 B; an odd
+// barrier count left them 8-B aligned: cudaErrorMisalignedAddress)
+__host__ __device__ constexpr size_t cl_tree_bytes_per_tree() {
+    return ((size_t)(2 * kTrUp + kTrDn + kTrOwn) * kTrStage + (size_t)kTrNbar * 8 + 16 + 127) & ~(size_t)127;
 }
-__host__ __device__ constexpr size_t cl_tree_bytes_per_tree() { return cl_tree_smem_bytes() / kTrTrees; }
+__host__ __device__ constexpr size_t cl_tree_smem_bytes() { return cl_tree_bytes_per_tree() * kTrTrees; }
+static_assert(kTrStage % 128 == 0, "tree stages must keep 128-B alignment");
 struct ClTreeSmem {
     uint32_t up[2], dn, own;            // inboxes (child k up, parent down), own stages
     uint32_t upfull[2], upempty;        // up inbox k landed / my up sends' credits
