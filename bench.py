@@ -490,6 +490,16 @@ def run_polar(args):
                              nccl_log)
     else:
         sweep = c2_sweep_virtual(L, comm, big, n, stream, t_step)
+        size_sweep = {"policy": "the active table (built-in default unless --policy): NVLink-oriented, "
+                                "one-shot below 1 MiB (DESIGN.md §4)",
+                      "sizes": size_sweep_virtual(L, comm, n, stream, peak)}
+        tuned = os.path.join(ROOT, "policies", "b200_virtual.json")
+        if os.path.exists(tuned) and not args.policy:
+            with open(tuned) as f:
+                rows = [tuple(r) for r in json.load(f)["rows"]]
+            size_sweep["tuned_virtual"] = {
+                "policy": "policies/b200_virtual.json (per-size choice measured on virtual ranks)",
+                "sizes": size_sweep_virtual(L, comm, n, stream, peak, table=rows)}
     comm.check()
     # virtual N=1: every algorithm's Simple kernel at the C2 size against the
     # same HBM roofline (ring / tree on both transports: clusters, and the
@@ -574,6 +584,8 @@ def run_polar(args):
         }
         if algos is not None:
             out["algorithms"] = algos
+        if not real:
+            out["size_sweep"] = size_sweep
         if ll128_probe is not None:
             out["ll128_probe"] = ll128_probe
         if unreg is not None:
@@ -737,6 +749,49 @@ def c2_sweep_virtual(L, comm, big, n, stream, t_step):
                         "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
                         "launched_channels": comm.launched_channels(),
                         "l2": "flushed before every call" if flushed else "n x S > 2 x L2, back to back"}
+    return out
+
+
+def size_sweep_virtual(L, comm, n, stream, peak, table=None):
+    """north_star's size range at N = 1: 4 KiB - 1 GiB per rank (x4 steps), 8
+    virtual ranks, f32 sum, policy-selected; algBW, busBW and the fraction of
+    the HBM copy peak by the 2 n S yardstick.  Points with n S <= 2 x L2 are
+    timed one call at a time after an L2 flush (no L2-resident number);
+    larger ones back to back."""
+    import torch
+    sizes = [(4 << 10) << (2 * k) for k in range(10)]
+    top = max(sizes)
+    saved = None
+    if table is not None:
+        saved = L.get_policy()[0]
+        L.set_policy(table)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    big = torch.zeros(n * (top // 4), dtype=torch.float32, device="cuda")
+    sptr = stream.cuda_stream
+    out = {}
+    for sz in sizes:
+        cnt = sz // 4
+        ptrs = [big[r * (top // 4):].data_ptr() for r in range(n)]
+
+        def call():
+            st = comm.allreduce_raw(ptrs, cnt, L.FLOAT32, L.SUM, sptr)
+            if st != 0:
+                raise L.PolarError(st, "polar_allreduce_v")
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        flushed = n * sz <= 2 * L2_BYTES
+        it = 20 if flushed else max(5, min(20, int(0.05 / (2 * n * sz / 6e12))))
+        t = _time_calls(call, it, stream, flush=(lambda: flush_buf.zero_()) if flushed else None)
+        d = comm.last_decision()
+        out[str(sz)] = {"algbw_gbs": round(sz / t / 1e9, 2), "busbw_gbs": round(busbw(sz, n, t), 2),
+                        "us": round(t * 1e6, 2), "hbm_frac": round(2 * n * sz / t / 1e9 / peak, 4),
+                        "decision": [L.ALGO_NAMES[d.algo], L.PROTO_NAMES[d.proto], d.nchannels],
+                        "l2": "flushed before every call" if flushed else "n x S > 2 x L2, back to back"}
+    del big, flush_buf
+    torch.cuda.empty_cache()
+    if saved is not None:
+        L.set_policy(saved)
     return out
 
 

@@ -65,7 +65,8 @@ def test_bench_torchrun_two_ranks_shared_gpu():
 
 def test_bench_single_gpu_line():
     """N = 1 (the driver's default run): the line carries parity, the L2-labelled
-    C2 sweep, the PCIe-bounded e2e and the CPU model."""
+    C2 sweep, the 4 KiB - 1 GiB size sweep (active and tuned tables), the
+    PCIe-bounded e2e and the CPU model."""
     env = dict(os.environ, POLAR_TIMEOUT_MS="20000")
     r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3"], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=900)
@@ -76,6 +77,14 @@ def test_bench_single_gpu_line():
     assert d["roofline"]["bound"] == "hbm" and d["gpu_launches"] == 5
     for sz, rec in d["c2_sweep"].items():
         assert rec["l2"].startswith("flushed") == (8 * int(sz) <= 2 * (126 << 20))
+    # north_star's size range at N = 1: 4 KiB - 1 GiB, active table and the tuned virtual table
+    for series in (d["size_sweep"]["sizes"], d["size_sweep"]["tuned_virtual"]["sizes"]):
+        assert [int(k) for k in series] == [(4 << 10) << (2 * k) for k in range(10)]
+        for sz, rec in series.items():
+            bus = 2 * 7 / 8 * int(sz) / (rec["us"] * 1e-6) / 1e9      # busBW = S * 2(n-1)/n / t
+            assert rec["us"] > 0 and abs(rec["busbw_gbs"] - bus) <= 0.01 + 1e-3 * bus, (sz, rec)
+            assert abs(rec["algbw_gbs"] - bus / 1.75) <= 0.01 + 1e-3 * bus, (sz, rec)
+            assert rec["l2"].startswith("flushed") == (8 * int(sz) <= 2 * (126 << 20))
 
 
 def test_nccl_variants_script():
