@@ -79,6 +79,9 @@ namespace dev {
 #define POLAR_CL_OWN 4            // (3: 128 MiB f32 685 us, 4: 650 us; profiles/r02y_cluster_ring_ab.jsonl)
 #endif
 #endif
+#ifndef POLAR_CL_JITTER
+#define POLAR_CL_JITTER 1         // fault injection point in the ring's tile loop (0 off, 1 before, 2 after the sends)
+#endif
 #ifndef POLAR_CL_PF
 #define POLAR_CL_PF 0             // own tiles prefetched into L2 ahead of the TMA loads (0: off)
 #endif
@@ -300,7 +303,10 @@ __device__ __forceinline__ void cl_rendezvous(const Params& P, uint32_t fin, int
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
         for (int p = 0; p < n; ++p)
             if (p != r) cl_arrive_remote(cl_map(fin, (uint32_t)p));
-        if (!cl_try_wait(fin, 0)) cl_wait_slow(fin, 0, P.timeout_ns, P.err, 0);
+        // (3x the loop timeout: a straggler that timed out in its loop arrives
+        // up to one timeout late; giving up at the same moment would let this
+        // CTA leave just before the straggler's fin arrive lands in it)
+        if (!cl_try_wait(fin, 0)) cl_wait_slow(fin, 0, 3 * P.timeout_ns, P.err, 0);
     }
     __syncthreads();
 }
@@ -475,6 +481,15 @@ struct ClCompute {
             const unsigned npk = (unsigned)((ke - i0) < TP ? (ke - i0) : TP);
             if (RECV && !cl_wait(P, S.full + 8u * xi, pi)) return false;
             if (OWN && !cl_wait(P, S.ofull + 8u * xw, pw)) return false;
+            // The credit.  Every sender warp also arrives on the successor's
+            // `full` barrier after its tile (below), so the successor cannot
+            // consume tile t — and credit stage t mod D again — before every one
+            // of my warps has passed its credit wait for tile t.  Without those
+            // arrivals a warp with no packs in a short tile could fall a whole
+            // stage reuse behind the credits, and its parity wait on `empty`
+            // would alias the phase it wants with the one after it and wait for
+            // a credit that never comes (found by tests/test_gpu_stress.py:
+            // n = 8, a few packs per sub-chunk, fault-injection delays).
             if (SEND && wrapped && !cl_wait(P, S.empty + 8u * xo, pe)) return false;
             uint32_t xa = 0;
             if constexpr (STAGE) {
@@ -488,13 +503,15 @@ struct ClCompute {
             const uint32_t dst = STAGE ? S.agst + xa * (uint32_t)kClStageBytes : dst_inbox + xo * (uint32_t)kClStageBytes;
             const uint32_t dbar = dst_full + 8u * xo;
             uint4* gout = mine + i0;
-            if (SEND) jitter_warp(P);
+            if (SEND && POLAR_CL_JITTER == 1) jitter_warp(P);
             if (npk == TP) body<KIND, true>(in, ow, dst, dbar, gout, npk);
             else body<KIND, false>(in, ow, dst, dbar, gout, npk);
+            if (SEND && POLAR_CL_JITTER == 2) jitter_warp(P);
             if constexpr (STAGE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // -> the bulk store
             __syncwarp();
             if ((me & 31u) == 0) {
                 if (RECV) mbar_arrive_u32(S.cons + 8u * xi);   // my reads of the inbox stage are done
+                if (SEND) cl_arrive_remote(dbar);   // this warp is past the tile's credit wait
                 if (OWN) mbar_arrive_u32(S.oempty + 8u * xw);
                 if (STAGE) mbar_arrive_rel_u32(S.finfull + 8u * xa);
             }
@@ -746,7 +763,7 @@ __global__ void __launch_bounds__(kClThreads, POLAR_CL_MINB) ring_cluster_kernel
     };
     if (threadIdx.x == 0) {
         for (int x = 0; x < kClStages; ++x) {
-            mbar_init_u32(S.full + 8u * x, 1);
+            mbar_init_u32(S.full + 8u * x, 1 + kClWarps);   // the signal warp's expect_tx + every sender warp
             mbar_init_u32(S.cons + 8u * x, kClWarps);
             mbar_init_u32(S.empty + 8u * x, 1);
         }
