@@ -126,3 +126,26 @@ def test_multiprocess_autoreg_cache_and_agreement(tmp_path, vmm_rank):
     tags = {x["tag"] for x in res}
     assert ({"cache/stats", "mixed-registration/auto", "decision-mismatch/estate"} <= tags) if vmm_rank is None \
         else ("vmm/stats" in tags)
+
+
+@pytest.mark.parametrize("jitter", ["0", "3000"])
+def test_multiprocess_random_stress(tmp_path, jitter):
+    """Time-bounded random stress of the real-comm path (3 processes, CUDA IPC):
+    forced algorithm x protocol or policy-selected, registered / unregistered /
+    auto-registered buffers, back-to-back batches; every result bit-exact
+    (tests/mp_worker_stress.py)."""
+    out = tmp_path / "stress.json"
+    env = dict(os.environ)
+    env.setdefault("POLAR_TIMEOUT_MS", "60000")
+    env.setdefault("POLAR_STRESS_S", "40")
+    env["POLAR_JITTER_NS"] = jitter
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "tests", "mp_worker_stress.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-4000:]
+    rep = json.loads(out.read_text())
+    assert all(x["calls"] == rep[0]["calls"] and x["calls"] > 0 for x in rep)
+    bad = [b for x in rep for b in x["bad"]]
+    assert not bad, bad[:20]
+    print({"calls": rep[0]["calls"], "kinds": len(rep[0]["kinds"])})
