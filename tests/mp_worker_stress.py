@@ -47,6 +47,11 @@ def main():
         return o
 
     comm = L.Comm.init(ws, rank, dev, L.torch_allgather(dist, ws))
+    if os.environ.get("POLAR_STRESS_POLICY"):
+        # ranks sharing one GPU under MPS: a table that caps the channels so every
+        # rank's CTAs stay co-resident (policies/mps_cap16.json)
+        with open(os.environ["POLAR_STRESS_POLICY"]) as f:
+            L.set_policy([tuple(r) for r in json.load(f)["rows"]])
     torn, reads = comm.probe_ll128(iters=500)      # real comms accept LL128 once probed
     (sym,) = comm.mem_alloc_tensors(SYM_BYTES // 4, torch.float32)
     rng = np.random.default_rng(int(os.environ.get("POLAR_STRESS_SEED", "2603")))
