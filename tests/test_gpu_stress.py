@@ -2,7 +2,8 @@
 (POLAR_STRESS_S seconds, default 45): random n, dtype, op, algorithm x
 protocol (ring / tree Simple run as clusters where eligible, the peer-memory
 FIFO kernels otherwise), element counts (whole packs and ragged), channel
-counts and buffer offsets, issued in back-to-back batches of 6 calls on one
+counts and buffer offsets, issued in back-to-back batches of 6 calls (a fifth of them direct ReduceScatter /
+AllGather / Broadcast) on one
 stream with no host synchronisation in between, half of the comms with
 random fault-injection delays.  Integer-valued inputs make every algorithm's
 result exact, so each call is compared bitwise with the oracle.  A rare race
@@ -24,6 +25,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from oracle import allreduce as orc  # noqa: E402
+from oracle import collectives as ocol  # noqa: E402
 from paper_2603_11438_b200 import polar as L  # noqa: E402
 
 ALGOS = ("oneshot", "twoshot", "ring", "tree")
@@ -60,6 +62,29 @@ def test_random_back_to_back_stress(monkeypatch):
                     off = int(rng.integers(2)) * int(rng.integers(1, per))   # element offset: unaligned start
                     nch = int(rng.integers(1, 33))
                     xs = synth.gen_ranks(dtype, count, n, cfg=int(rng.integers(1 << 30)), dist="ints")
+                    if int(rng.integers(5)) == 0 and count >= n:
+                        # a direct ReduceScatter / AllGather / Broadcast in the same stream
+                        coll = ("rs", "ag", "bc")[int(rng.integers(3))]
+                        blk = max(1, count // n)
+                        if coll == "rs":
+                            xr = [x[:blk * n] for x in xs]
+                            snd = [to_device(x, dtype) for x in xr]
+                            rcv = [to_device(np.zeros(blk, dtype=x.dtype), dtype) for x in xr]
+                            c.reduce_scatter(snd, rcv, op=op)
+                            pending.append(("rs", xr, rcv, dtype, op, None))
+                        elif coll == "ag":
+                            xa = [x[:blk] for x in xs]
+                            snd = [to_device(x, dtype) for x in xa]
+                            rcv = [to_device(np.zeros(blk * n, dtype=x.dtype), dtype) for x in xa]
+                            c.all_gather(snd, rcv)
+                            pending.append(("ag", xa, rcv, dtype, op, None))
+                        else:
+                            root = int(rng.integers(n))
+                            bts = [to_device(x, dtype) for x in xs]
+                            c.broadcast(bts, root=root)
+                            pending.append(("bc", xs, bts, dtype, op, root))
+                        stats[(coll,)] = stats.get((coll,), 0) + 1
+                        continue
                     ts = [to_device(x, dtype, offset=off) for x in xs]
                     if debug:
                         print("call", n, jitter, dtype, op, algo, proto, count, nch, off, flush=True)
@@ -72,7 +97,23 @@ def test_random_back_to_back_stress(monkeypatch):
                     pending.append((xs, ts, dtype, op, key, count, nch, off))
                 torch.cuda.synchronize()
                 c.check()
-                for xs, ts, dtype, op, key, count, nch, off in pending:
+                for item in pending:
+                    if isinstance(item[0], str):
+                        coll, xs, outs, dtype, op, root = item
+                        if coll == "rs":
+                            exps = ocol.reduce_scatter(xs, dtype, op)
+                        elif coll == "ag":
+                            exps = [ocol.all_gather(xs)] * n
+                        else:
+                            exps = [ocol.broadcast(xs, root)] * n
+                        for r, (t, e) in enumerate(zip(outs, exps)):
+                            got = to_host(t, dtype)
+                            ok = np.array_equal(got, e) if (dtype == "f32" and op != "sum" and coll == "rs") else \
+                                np.array_equal(got.view(np.uint8), np.asarray(e).view(np.uint8))
+                            assert ok, (n, coll, dtype, op, len(xs[0]), r)
+                        calls += 1
+                        continue
+                    xs, ts, dtype, op, key, count, nch, off = item
                     exp = orc.allreduce(xs, dtype, op)
                     for r, t in enumerate(ts):
                         got = to_host(t, dtype)
@@ -82,5 +123,6 @@ def test_random_back_to_back_stress(monkeypatch):
                     calls += 1
         finally:
             c.destroy()
-    print(f"stress: {calls} calls checked in {budget:.0f} s, {clusters} as clusters; {sorted(stats.items())}")
+    print(f"stress: {calls} calls checked in {budget:.0f} s, {clusters} as clusters; "
+          f"{sorted(stats.items(), key=str)}")
     assert calls > 0
