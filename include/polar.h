@@ -206,7 +206,13 @@ polar_status polar_bench_swap(uint32_t nthreads, uint64_t calls_per_thread, uint
  * §3(4)).  Allocates this rank's symmetric scratch (flags + staging) on
  * cuda_device, exchanges CUDA IPC handles through `ag` (the only host
  * collective), maps every peer's scratch and runs a device handshake.
- * Collective.  nranks 1..8, 0 <= rank < nranks. */
+ * Collective.  nranks 1..8, 0 <= rank < nranks.  Ranks that share one GPU
+ * (several processes per device, e.g. under MPS) are detected from the GPU
+ * UUIDs: programmatic dependent launch is then off, and every launch's channel
+ * count is capped at the device's co-resident CTAs / the ranks per GPU (the
+ * minimum over ranks), so that every rank's CTAs can be resident together —
+ * polar_comm_last_decision still reports the policy's decision,
+ * polar_comm_launch_info what was launched.  One rank per GPU: no cap. */
 polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_device,
                              polar_allgather_fn ag, void* user);
 

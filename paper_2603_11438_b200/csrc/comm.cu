@@ -134,6 +134,7 @@ struct polar_comm_s {
     void* user = nullptr;
     uint64_t init_value = 0;
     int max_coop_blocks = 0;             // virtual: co-residency bound
+    int share_cap = 0;                   // real comm with ranks sharing a GPU: channel cap (0: none)
     unsigned long long* trace = nullptr; // diagnostic per-CTA timestamps
     bool coop = true;                    // virtual: cooperative launch (co-residency guaranteed)
     bool pdl = true;                     // programmatic dependent launch (POLAR_PDL=0 disables)
@@ -763,6 +764,26 @@ polar_status autoreg_map(polar_comm_s* c, char* mine, size_t bytes, uint64_t dta
     return POLAR_OK;
 }
 
+// Co-residency bound of a launch on one device: SMs x the fewest CTAs per SM
+// of any AllReduce kernel we may launch (virtual comms clamp their grids to it;
+// real comms whose ranks share a GPU divide it among those ranks).
+polar_status coresident_blocks(int cuda_device, int* blocks) {
+    int sms = 0, per_sm = 0, minper = 1 << 30;
+    polar_status st = cuerr(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
+    const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
+    const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
+    const int algos[] = {POLAR_ALGO_TREE, POLAR_ALGO_RING, POLAR_ALGO_ONESHOT, POLAR_ALGO_TWOSHOT};
+    const int protos[] = {POLAR_PROTO_LL, POLAR_PROTO_LL128, POLAR_PROTO_SIMPLE};
+    for (int dt : dts) for (int op : ops) for (int a : algos) for (int pr : protos) {
+        if (st != POLAR_OK) break;
+        const void* fn = kernel_for(dt, op, a, pr);
+        st = cuerr(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kBlock, 0));
+        minper = std::min(minper, per_sm);
+    }
+    *blocks = sms * minper;
+    return st;
+}
+
 struct BootRec {
     uint64_t magic;
     uint32_t nranks, rank;
@@ -784,7 +805,8 @@ uint64_t layout_hash(const Layout& L) {
 // uuid: this rank's GPU (may be null); *shared_gpu (may be null) is set when
 // another rank reports the same GPU (several ranks on one device, e.g. MPS).
 polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgather_fn ag, void* user,
-                             const unsigned char* uuid = nullptr, bool* shared_gpu = nullptr) {
+                             const unsigned char* uuid = nullptr, bool* shared_gpu = nullptr,
+                             int* max_per_gpu = nullptr) {
     BootRec mine{kBootMagic, (uint32_t)nranks, (uint32_t)rank, layout_hash(L), 0, {}};
     if (uuid) std::memcpy(mine.uuid, uuid, sizeof(mine.uuid));
     std::vector<BootRec> all(nranks);
@@ -798,6 +820,16 @@ polar_status bootstrap_check(int nranks, int rank, const Layout& L, polar_allgat
         if (p != rank && std::memcmp(r.uuid, mine.uuid, sizeof(mine.uuid)) == 0) shared = true;
     }
     if (shared_gpu) *shared_gpu = shared;
+    if (max_per_gpu) {
+        // the most ranks any one GPU hosts (the same on every rank: gathered data)
+        int most = 1;
+        for (int p = 0; p < nranks; ++p) {
+            int k = 0;
+            for (int q = 0; q < nranks; ++q) k += std::memcmp(all[p].uuid, all[q].uuid, sizeof(mine.uuid)) == 0;
+            most = std::max(most, k);
+        }
+        *max_per_gpu = most;
+    }
     return POLAR_OK;
 }
 
@@ -899,6 +931,8 @@ polar_status do_allreduce(polar_comm_s* c, void* const* bufs, size_t count, int 
     } else if (c->is_virtual) {
         const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;   // co-residency bound
+    } else if (c->share_cap > 0 && (int)d.nchannels > c->share_cap) {
+        d.nchannels = (uint32_t)c->share_cap;                          // ranks sharing a GPU
     }
     c->last_nch = d.nchannels;        // what is launched
     c->last_transport = use_cluster ? POLAR_TRANSPORT_CLUSTER : POLAR_TRANSPORT_PEER;
@@ -1109,6 +1143,8 @@ polar_status do_direct(polar_comm_s* c, int mode, void* const* sends, void* cons
     if (c->is_virtual) {
         const int maxch = std::max(1, c->max_coop_blocks / c->nranks);
         if ((int)d.nchannels > maxch) d.nchannels = (uint32_t)maxch;
+    } else if (c->share_cap > 0 && (int)d.nchannels > c->share_cap) {
+        d.nchannels = (uint32_t)c->share_cap;
     }
     c->last_nch = d.nchannels;
     c->last_transport = POLAR_TRANSPORT_PEER;
@@ -1196,9 +1232,24 @@ polar_status polar_comm_init(polar_comm_t* out, int nranks, int rank, int cuda_d
     cudaDeviceProp prop{};
     if (st == POLAR_OK) st = cuerr(cudaGetDeviceProperties(&prop, cuda_device));
     bool shared_gpu = false;
+    int per_gpu = 1;
     if (st == POLAR_OK)
         st = bootstrap_check(nranks, rank, c->L, ag, user, reinterpret_cast<const unsigned char*>(prop.uuid.bytes),
-                             &shared_gpu);
+                             &shared_gpu, &per_gpu);
+    // Ranks sharing one GPU (MPS): every rank's CTAs must be resident together
+    // or the cross-rank waits cannot complete, so the channel count is capped at
+    // the co-resident CTAs / the ranks per GPU (the same cap on every rank: the
+    // minimum over ranks); one rank per GPU (a node) has no cap.
+    if (st == POLAR_OK && per_gpu > 1) {
+        int blocks = 0;
+        st = coresident_blocks(cuda_device, &blocks);
+        uint32_t mine = (uint32_t)std::max(1, blocks / per_gpu), all[kMaxRanks];
+        if (st == POLAR_OK && ag(&mine, all, sizeof(mine), user) != 0) st = POLAR_ESTATE;
+        if (st == POLAR_OK) {
+            for (int p = 0; p < nranks; ++p) mine = std::min(mine, all[p]);
+            c->share_cap = (int)mine;
+        }
+    }
     // Ranks sharing one GPU (MPS) must not use programmatic dependent launch: a
     // rank's pre-launched next kernels can hold the SMs another rank's CURRENT
     // kernel needs, and the cross-rank waits then never complete (measured: 4
@@ -1254,20 +1305,7 @@ polar_status polar_comm_init_virtual(polar_comm_t* out, int nranks, int cuda_dev
         c->scratch[p] = c->scratch_own[p];
     }
     if (st == POLAR_OK) {
-        // co-residency bound for the cooperative launch (smallest over all kernels we may launch)
-        int sms = 0, per_sm = 0, minper = 1 << 30;
-        st = cuerr(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
-        const int dts[] = {POLAR_INT32, POLAR_INT64, POLAR_FLOAT32, POLAR_BFLOAT16};
-        const int ops[] = {POLAR_SUM, POLAR_MAX, POLAR_MIN};
-        const int algos[] = {POLAR_ALGO_TREE, POLAR_ALGO_RING, POLAR_ALGO_ONESHOT, POLAR_ALGO_TWOSHOT};
-        const int protos[] = {POLAR_PROTO_LL, POLAR_PROTO_LL128, POLAR_PROTO_SIMPLE};
-        for (int dt : dts) for (int op : ops) for (int a : algos) for (int pr : protos) {
-            if (st != POLAR_OK) break;
-            const void* fn = kernel_for(dt, op, a, pr);
-            st = cuerr(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kBlock, 0));
-            minper = std::min(minper, per_sm);
-        }
-        c->max_coop_blocks = sms * minper;
+        st = coresident_blocks(cuda_device, &c->max_coop_blocks);
         if (st == POLAR_OK && c->max_coop_blocks < nranks) st = POLAR_EUNSUPPORTED;
     }
     if (st == POLAR_OK && nranks > 1) {
